@@ -1,0 +1,43 @@
+# Builds everything in-tree (the .so files travel to the GPU box with gpurun).
+#   make            -> product library + oracle (+ oracle/_ref when the reference is present)
+#   make lib        -> paper_2304_08662_b200/_lib/libxdrop_b200.so  (sm_100a)
+NVCC ?= /usr/local/cuda/bin/nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 -Xptxas -v
+CSRC := paper_2304_08662_b200/csrc
+LIB := paper_2304_08662_b200/_lib/libxdrop_b200.so
+OBJDIR := build
+
+SRCS_CU := $(CSRC)/xb_kernels.cu $(CSRC)/xb_engine.cu
+SRCS_CPP := $(CSRC)/xb_synth.cpp
+HDRS := $(CSRC)/xb_internal.h $(CSRC)/xb_kernels.cuh include/xdrop_b200.h
+
+all: lib oracle
+
+lib: $(LIB)
+
+$(OBJDIR)/xb_kernels.o: $(CSRC)/xb_kernels.cu $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -dc -o $@ $< 2> $(OBJDIR)/xb_kernels.ptxas.txt || (cat $(OBJDIR)/xb_kernels.ptxas.txt; exit 1)
+
+$(OBJDIR)/xb_engine.o: $(CSRC)/xb_engine.cu $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -dc -o $@ $< 2> $(OBJDIR)/xb_engine.ptxas.txt || (cat $(OBJDIR)/xb_engine.ptxas.txt; exit 1)
+
+$(OBJDIR)/xb_synth.o: $(CSRC)/xb_synth.cpp include/xdrop_b200.h
+	@mkdir -p $(OBJDIR)
+	/usr/bin/g++ -O3 -std=c++17 -fPIC -c -o $@ $<
+
+$(LIB): $(OBJDIR)/xb_kernels.o $(OBJDIR)/xb_engine.o $(OBJDIR)/xb_synth.o
+	@mkdir -p $(dir $(LIB))
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^ -lpthread
+
+oracle:
+	$(MAKE) -s -C oracle liboracle.so
+	@if [ -d /root/reference/proj/src ]; then $(MAKE) -s -C oracle ref; fi
+
+clean:
+	rm -rf $(OBJDIR) $(LIB)
+	$(MAKE) -C oracle clean
+
+.PHONY: all lib oracle clean

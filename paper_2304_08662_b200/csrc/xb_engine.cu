@@ -1,0 +1,1117 @@
+// Host side of the xdrop_b200 C-ABI: scoring schemes, the detached sequence
+// pool (2-bit / 5-bit packing, one upload per device), LR split + cost sort
+// on the device, the tier cascade, and LPT sharding across devices.
+// Reference interfaces replaced are cited per entry point in
+// include/xdrop_b200.h.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <numeric>
+#include <queue>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
+
+#include "../../include/xdrop_b200.h"
+#include "xb_internal.h"
+#include "xb_kernels.cuh"
+
+namespace xb {
+template <int K, int MODE>
+__global__ void thread_tier_kernel(TierParams P);
+template <int ENC>
+__global__ void warp_tier_kernel(TierParams P);
+__global__ void prep_kernel(PrepParams P);
+__global__ void int_peak_alu(int32_t* out, int iters, int32_t seed, long long* clk);
+__global__ void int_peak_mixed(int32_t* out, int iters, int32_t seed, long long* clk);
+
+
+}  // namespace xb
+
+using namespace xb;
+
+namespace {
+
+thread_local xb_stats g_last_stats{};
+
+#define CK(call)                                                                      \
+    do {                                                                              \
+        cudaError_t e_ = (call);                                                      \
+        if (e_ != cudaSuccess) {                                                      \
+            std::fprintf(stderr, "xdrop_b200: %s failed: %s (%s:%d)\n", #call,        \
+                         cudaGetErrorString(e_), __FILE__, __LINE__);                 \
+            return XB_E_CUDA;                                                         \
+        }                                                                             \
+    } while (0)
+
+int n_host_threads() {
+    unsigned h = std::thread::hardware_concurrency();
+    return int(std::max(1u, std::min(h, 64u)));
+}
+
+template <class F>
+void parallel_for(int64_t n, F&& f) {
+    const int T = n > (1 << 16) ? n_host_threads() : 1;
+    if (T <= 1) {
+        f(int64_t(0), n);
+        return;
+    }
+    std::vector<std::thread> th;
+    const int64_t chunk = (n + T - 1) / T;
+    for (int t = 0; t < T; ++t) {
+        const int64_t a = t * chunk, b = std::min(n, a + chunk);
+        if (a < b) th.emplace_back([&f, a, b] { f(a, b); });
+    }
+    for (auto& x : th) x.join();
+}
+
+}  // namespace
+
+// ----------------------------------------------------------------- scheme ----
+
+struct xb_scheme {
+    int kind = 0;  // 0 match/mismatch, 1 matrix
+    int match = 0, mismatch = 0, gap = -1, x = 0;
+    std::string alphabet;
+    std::vector<int> cells;  // n*n
+    int16_t table[256 * 256];
+    bool valid[256];
+    int8_t code_of[256];
+};
+
+extern "C" {
+
+const char* xb_version(void) { return "xdrop_b200 0.1 (sm_100a)"; }
+
+const char* xb_strerror(int code) {
+    switch (code) {
+        case XB_OK: return "ok";
+        case XB_E_BAD_PARAM: return "invalid parameter";
+        case XB_E_DANGLING: return "task references an unknown sequence";
+        case XB_E_SEED_OOB: return "seed does not fit inside its sequences";
+        case XB_E_UNKNOWN_SYMBOL: return "symbol not in scoring alphabet";
+        case XB_E_OUT_OF_RANGE: return "view out of range";
+        case XB_E_CUDA: return "CUDA error";
+        case XB_E_NO_DEVICE: return "no CUDA device";
+        case XB_E_PARSE: return "malformed substitution matrix";
+        default: return "unknown error";
+    }
+}
+
+int xb_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+static void scheme_finish(xb_scheme* s) {
+    std::memset(s->table, 0, sizeof s->table);
+    std::memset(s->valid, 0, sizeof s->valid);
+    std::memset(s->code_of, -1, sizeof s->code_of);
+    const int n = int(s->alphabet.size());
+    for (int i = 0; i < n; ++i) {
+        const unsigned char a = (unsigned char)s->alphabet[size_t(i)];
+        s->valid[a] = true;
+        s->code_of[a] = int8_t(i);  // last occurrence wins, like the table
+        for (int j = 0; j < n; ++j) {
+            const unsigned char b = (unsigned char)s->alphabet[size_t(j)];
+            s->table[a * 256 + b] = int16_t(s->cells[size_t(i * n + j)]);
+        }
+    }
+}
+
+xb_scheme* xb_scheme_match_mismatch(int match, int mismatch, int gap, int x, int* err) {
+    if (match <= 0 || mismatch >= 0 || gap >= 0 || x < 0) {
+        if (err) *err = XB_E_BAD_PARAM;
+        return nullptr;
+    }
+    auto* s = new xb_scheme();
+    s->kind = 0;
+    s->match = match;
+    s->mismatch = mismatch;
+    s->gap = gap;
+    s->x = x;
+    s->alphabet = "ACGTN";
+    s->cells.assign(25, mismatch);
+    for (int i = 0; i < 4; ++i) s->cells[size_t(i * 5 + i)] = match;  // N never matches
+    scheme_finish(s);
+    if (err) *err = XB_OK;
+    return s;
+}
+
+xb_scheme* xb_scheme_from_matrix(const char* alphabet, int n, const int* cells, int gap, int x,
+                                 int* err) {
+    if (gap >= 0 || x < 0 || n <= 0 || n > 31 || !alphabet || !cells) {
+        if (err) *err = XB_E_BAD_PARAM;
+        return nullptr;
+    }
+    auto* s = new xb_scheme();
+    s->kind = 1;
+    s->gap = gap;
+    s->x = x;
+    s->alphabet.assign(alphabet, size_t(n));
+    s->cells.assign(cells, cells + size_t(n) * size_t(n));
+    scheme_finish(s);
+    if (err) *err = XB_OK;
+    return s;
+}
+
+int xb_parse_submatrix(const char* text, char* alphabet_out, int alphabet_cap, int* cells_out,
+                       int cells_cap) {
+    if (!text) return -XB_E_BAD_PARAM;
+    std::string alpha, labels;
+    std::vector<std::vector<int>> rows;
+    const char* p = text;
+    while (*p) {
+        const char* e = std::strchr(p, '\n');
+        std::string line = e ? std::string(p, size_t(e - p)) : std::string(p);
+        p = e ? e + 1 : p + line.size();
+        if (!line.empty() && line.back() == '\r') line.pop_back();
+        const size_t pos = line.find_first_not_of(" \t");
+        if (pos == std::string::npos || line[pos] == '#') continue;
+        // whitespace tokens
+        std::vector<std::string> tok;
+        size_t q = 0;
+        while (q < line.size()) {
+            while (q < line.size() && (line[q] == ' ' || line[q] == '\t')) ++q;
+            size_t r = q;
+            while (r < line.size() && line[r] != ' ' && line[r] != '\t') ++r;
+            if (r > q) tok.push_back(line.substr(q, r - q));
+            q = r;
+        }
+        if (alpha.empty()) {
+            for (auto& t : tok) {
+                if (t.size() != 1) return -XB_E_PARSE;
+                alpha += t;
+            }
+            continue;
+        }
+        if (tok.empty() || tok[0].size() != 1) return -XB_E_PARSE;
+        std::vector<int> row;
+        for (size_t i = 1; i < tok.size(); ++i) {
+            char* end = nullptr;
+            const long v = std::strtol(tok[i].c_str(), &end, 10);
+            if (end == tok[i].c_str() || *end) break;  // istream >> int stops here
+            row.push_back(int(v));
+        }
+        if (row.size() != alpha.size()) return -XB_E_PARSE;
+        labels += tok[0];
+        rows.push_back(std::move(row));
+    }
+    if (alpha.empty() || rows.size() != alpha.size() || labels != alpha) return -XB_E_PARSE;
+    const int n = int(alpha.size());
+    if (n + 1 > alphabet_cap || n * n > cells_cap) return -XB_E_BAD_PARAM;
+    std::memcpy(alphabet_out, alpha.data(), size_t(n));
+    alphabet_out[n] = 0;
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) cells_out[i * n + j] = rows[size_t(i)][size_t(j)];
+    return n;
+}
+
+int xb_scheme_sim(const xb_scheme* s, char a, char b, int* out) {
+    if (!s->valid[(unsigned char)a] || !s->valid[(unsigned char)b]) return XB_E_UNKNOWN_SYMBOL;
+    *out = s->table[(unsigned char)a * 256 + (unsigned char)b];
+    return XB_OK;
+}
+
+void xb_scheme_free(xb_scheme* s) { delete s; }
+
+}  // extern "C"
+
+// ------------------------------------------------------------------- pool ----
+
+struct DevPool {
+    uint32_t* words = nullptr;
+    int64_t* seq_pos = nullptr;
+    int64_t* seq_len = nullptr;
+    DevScheme* scheme = nullptr;
+    bool ready = false;
+};
+
+struct xb_pool {
+    xb_scheme scheme;
+    std::vector<char> symbols;
+    std::vector<int64_t> offsets{0};
+    bool all_acgt = true;
+    // packed host image
+    bool packed = false;
+    int enc = ENC_2BIT;
+    uint32_t* host_words = nullptr;  // pinned
+    int64_t n_words = 0;
+    std::vector<int64_t> seq_pos, seq_len;
+    DevScheme dev_scheme{};
+    std::map<int, DevPool> dev;
+    std::mutex mu;
+};
+
+static bool fast_dna(const xb_pool* p) {
+    return p->enc == ENC_2BIT && p->scheme.kind == 0 && p->scheme.match == 1 &&
+           p->scheme.mismatch == -1 && p->scheme.gap == -1;
+}
+
+// Admits the drift-space thread tiers for this scheme (DESIGN.md guards).
+static bool thread_tiers_ok(const xb_pool* p) {
+    const xb_scheme& s = p->scheme;
+    if (s.gap <= -(1 << 10) || s.x >= (1 << 22)) return false;
+    if (fast_dna(p)) return true;
+    for (int v : s.cells) {
+        const long t = long(v) - 2L * s.gap;
+        if (t < -127 || t > 127) return false;
+    }
+    return true;
+}
+
+static void pool_pack(xb_pool* p) {
+    if (p->packed) return;
+    const xb_scheme& s = p->scheme;
+    p->enc = (s.kind == 0 && p->all_acgt) ? ENC_2BIT : ENC_5BIT;
+    const int64_t total = int64_t(p->symbols.size());
+    const int64_t nsym = kPoolPad + total + kPoolPad;
+    p->n_words = p->enc == ENC_2BIT ? (nsym + 15) / 16 + 2 : (nsym + 5) / 6 + 2;
+    if (p->host_words) cudaFreeHost(p->host_words);
+    if (cudaMallocHost(&p->host_words, size_t(p->n_words) * 4) != cudaSuccess) {
+        cudaGetLastError();
+        p->host_words = (uint32_t*)std::malloc(size_t(p->n_words) * 4);
+    }
+    uint8_t code[256];
+    for (int c = 0; c < 256; ++c) code[c] = 0;
+    if (p->enc == ENC_2BIT) {
+        code['A'] = 0;
+        code['C'] = 1;
+        code['G'] = 2;
+        code['T'] = 3;
+    } else {
+        for (int c = 0; c < 256; ++c) code[c] = s.code_of[c] < 0 ? 0 : uint8_t(s.code_of[c]);
+    }
+    const char* sym = p->symbols.data();
+    uint32_t* W = p->host_words;
+    const int per = p->enc == ENC_2BIT ? 16 : 6;
+    const int bits = p->enc == ENC_2BIT ? 2 : 5;
+    parallel_for(p->n_words, [&](int64_t a, int64_t b) {
+        for (int64_t w = a; w < b; ++w) {
+            uint32_t acc = 0;
+            const int64_t p0 = w * per;
+            for (int q = 0; q < per; ++q) {
+                const int64_t s0 = p0 + q - kPoolPad;
+                if (s0 >= 0 && s0 < total) acc |= uint32_t(code[(unsigned char)sym[s0]]) << (bits * q);
+            }
+            W[w] = acc;
+        }
+    });
+    const int64_t n = int64_t(p->offsets.size()) - 1;
+    p->seq_pos.resize(size_t(n));
+    p->seq_len.resize(size_t(n));
+    for (int64_t i = 0; i < n; ++i) {
+        p->seq_pos[size_t(i)] = kPoolPad + p->offsets[size_t(i)];
+        p->seq_len[size_t(i)] = p->offsets[size_t(i) + 1] - p->offsets[size_t(i)];
+    }
+    DevScheme& d = p->dev_scheme;
+    std::memset(&d, 0, sizeof d);
+    d.gap = s.gap;
+    d.x = s.x;
+    d.enc = p->enc;
+    d.fast_dna = fast_dna(p) ? 1 : 0;
+    d.max_score = INT32_MIN;
+    d.min_score = INT32_MAX;
+    const int na = int(s.alphabet.size());
+    for (int i = 0; i < 32 * 32; ++i) d.sim[i] = -(1 << 20);
+    if (p->enc == ENC_2BIT) {
+        const char* acgt = "ACGT";
+        for (int a = 0; a < 4; ++a)
+            for (int b = 0; b < 4; ++b)
+                d.sim[a * 32 + b] = s.table[(unsigned char)acgt[a] * 256 + (unsigned char)acgt[b]];
+    } else {
+        for (int a = 0; a < na; ++a)
+            for (int b = 0; b < na; ++b)
+                d.sim[a * 32 + b] = s.table[(unsigned char)s.alphabet[size_t(a)] * 256 +
+                                            (unsigned char)s.alphabet[size_t(b)]];
+    }
+    for (int v : s.cells) {
+        d.max_score = std::max(d.max_score, v);
+        d.min_score = std::min(d.min_score, v);
+    }
+    p->packed = true;
+}
+
+static int pool_device(xb_pool* p, int dev, cudaStream_t st, int64_t* h2d, DevPool** out) {
+    std::lock_guard<std::mutex> g(p->mu);
+    pool_pack(p);
+    DevPool& D = p->dev[dev];
+    if (!D.ready) {
+        CK(cudaSetDevice(dev));
+        const int64_t n = int64_t(p->seq_pos.size());
+        if (!D.words) {
+            CK(cudaMalloc(&D.words, size_t(p->n_words) * 4));
+            CK(cudaMalloc(&D.seq_pos, size_t(std::max<int64_t>(n, 1)) * 8));
+            CK(cudaMalloc(&D.seq_len, size_t(std::max<int64_t>(n, 1)) * 8));
+            CK(cudaMalloc(&D.scheme, sizeof(DevScheme)));
+        }
+        CK(cudaMemcpyAsync(D.words, p->host_words, size_t(p->n_words) * 4, cudaMemcpyHostToDevice, st));
+        if (n) {
+            CK(cudaMemcpyAsync(D.seq_pos, p->seq_pos.data(), size_t(n) * 8, cudaMemcpyHostToDevice, st));
+            CK(cudaMemcpyAsync(D.seq_len, p->seq_len.data(), size_t(n) * 8, cudaMemcpyHostToDevice, st));
+        }
+        CK(cudaMemcpyAsync(D.scheme, &p->dev_scheme, sizeof(DevScheme), cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));  // pageable sources above must outlive the copy
+        if (h2d) *h2d += p->n_words * 4 + n * 16 + int64_t(sizeof(DevScheme));
+        D.ready = true;
+    }
+    *out = &D;
+    return XB_OK;
+}
+
+static void pool_drop_devices(xb_pool* p) {
+    for (auto& kv : p->dev) {
+        cudaSetDevice(kv.first);
+        cudaFree(kv.second.words);
+        cudaFree(kv.second.seq_pos);
+        cudaFree(kv.second.seq_len);
+        cudaFree(kv.second.scheme);
+    }
+    p->dev.clear();
+}
+
+extern "C" {
+
+xb_pool* xb_pool_create(const xb_scheme* s, int* err) {
+    if (!s) {
+        if (err) *err = XB_E_BAD_PARAM;
+        return nullptr;
+    }
+    auto* p = new xb_pool();
+    p->scheme = *s;
+    if (err) *err = XB_OK;
+    return p;
+}
+
+int64_t xb_pool_add_bulk(xb_pool* p, const char* concat, const int64_t* offsets, int64_t n) {
+    if (!p || n < 0 || (n && (!concat || !offsets))) return -XB_E_BAD_PARAM;
+    const int64_t total = n ? offsets[n] - offsets[0] : 0;
+    // validate (io.cpp:82-89 ingestion rule) before touching the pool
+    std::atomic<int> bad{0};
+    std::atomic<bool> non_acgt{false};
+    const char* base = concat + (n ? offsets[0] : 0);
+    parallel_for(total, [&](int64_t a, int64_t b) {
+        bool na = false;
+        for (int64_t i = a; i < b; ++i) {
+            const unsigned char c = (unsigned char)base[i];
+            if (!p->scheme.valid[c]) {
+                bad = 1;
+                return;
+            }
+            na |= (c != 'A' && c != 'C' && c != 'G' && c != 'T');
+        }
+        if (na) non_acgt = true;
+    });
+    if (bad) return -XB_E_UNKNOWN_SYMBOL;
+    std::lock_guard<std::mutex> g(p->mu);
+    const int64_t first = int64_t(p->offsets.size()) - 1;
+    const int64_t at = int64_t(p->symbols.size());
+    p->symbols.resize(size_t(at + total));
+    std::memcpy(p->symbols.data() + at, base, size_t(total));
+    for (int64_t i = 0; i < n; ++i) p->offsets.push_back(at + offsets[i + 1] - offsets[0]);
+    if (non_acgt) p->all_acgt = false;
+    p->packed = false;
+    for (auto& kv : p->dev) kv.second.ready = false;
+    return first;
+}
+
+int64_t xb_pool_add(xb_pool* p, const char* symbols, int64_t len) {
+    const int64_t off[2] = {0, len};
+    return xb_pool_add_bulk(p, symbols, off, 1);
+}
+
+int64_t xb_pool_size(const xb_pool* p) { return int64_t(p->offsets.size()) - 1; }
+
+int64_t xb_pool_seq_len(const xb_pool* p, int64_t id) {
+    if (id < 0 || id >= xb_pool_size(p)) return -XB_E_DANGLING;
+    return p->offsets[size_t(id) + 1] - p->offsets[size_t(id)];
+}
+
+int xb_pool_bits_per_symbol(const xb_pool* p) {
+    return (p->scheme.kind == 0 && p->all_acgt) ? 2 : 5;
+}
+
+void xb_pool_evict(xb_pool* p) {
+    std::lock_guard<std::mutex> g(p->mu);
+    for (auto& kv : p->dev) kv.second.ready = false;
+}
+
+void xb_pool_free(xb_pool* p) {
+    if (!p) return;
+    pool_drop_devices(p);
+    if (p->host_words) cudaFreeHost(p->host_words);
+    delete p;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ batch ----
+
+struct DevBatch {
+    int dev = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    DevPool* pool = nullptr;
+    std::vector<int64_t> tasks;  // global task (or unit) indices of this shard
+    int64_t n_items = 0;         // tasks (or units) on this device
+    int64_t n_units = 0;
+    int64_t* d_tasks = nullptr;
+    DevUnit* d_units = nullptr;
+    uint32_t *d_keys = nullptr, *d_vals = nullptr, *d_keys2 = nullptr, *d_order = nullptr;
+    DevResult* d_res = nullptr;
+    int32_t* d_seed = nullptr;
+    uint32_t *d_list1 = nullptr, *d_list2 = nullptr;
+    DevCounters* d_ctr = nullptr;
+    int32_t* d_scratch = nullptr;
+    int scratch_warps = 0;
+    void* d_cub = nullptr;
+    size_t cub_bytes = 0;
+    cudaEvent_t ev[6] = {};
+    int sm_count = 0;
+    int occ[2] = {0, 0};
+    int launches = 0;
+    // host staging (pinned)
+    DevResult* h_res = nullptr;
+    int32_t* h_seed = nullptr;
+    // host-built units (units mode)
+    std::vector<DevUnit> h_units;
+};
+
+struct xb_batch {
+    xb_pool* pool = nullptr;
+    int k = 0, band = 0, flags = 0;
+    bool units_mode = false;
+    int64_t n = 0;
+    std::vector<DevBatch> devs;
+    int64_t h2d = 0, d2h = 0;
+    bool ran = false;
+};
+
+static void free_dev(DevBatch& D) {
+    cudaSetDevice(D.dev);
+    cudaFree(D.d_tasks);
+    cudaFree(D.d_units);
+    cudaFree(D.d_keys);
+    cudaFree(D.d_vals);
+    cudaFree(D.d_keys2);
+    cudaFree(D.d_order);
+    cudaFree(D.d_res);
+    cudaFree(D.d_seed);
+    cudaFree(D.d_list1);
+    cudaFree(D.d_list2);
+    cudaFree(D.d_ctr);
+    cudaFree(D.d_scratch);
+    cudaFree(D.d_cub);
+    for (auto& e : D.ev)
+        if (e) cudaEventDestroy(e);
+    if (D.own_stream && D.stream) cudaStreamDestroy(D.stream);
+    if (D.h_res) cudaFreeHost(D.h_res);
+    if (D.h_seed) cudaFreeHost(D.h_seed);
+}
+
+// longest-first estimate for a unit, shared with the prep kernel
+static inline long long unit_est(long long hl, long long vl) {
+    const long long mn = std::min(hl, vl);
+    const long long gd = hl > vl ? hl - vl : vl - hl;
+    return 2 * mn + std::min(gd, 64LL);
+}
+
+static int setup_device(xb_batch* B, DevBatch& D, const xb_exec* ex) {
+    CK(cudaSetDevice(D.dev));
+    if (ex && ex->stream && B->devs.size() == 1) {
+        D.stream = (cudaStream_t)ex->stream;
+    } else {
+        CK(cudaStreamCreateWithFlags(&D.stream, cudaStreamNonBlocking));
+        D.own_stream = true;
+    }
+    for (auto& e : D.ev) CK(cudaEventCreate(&e));
+    CK(cudaDeviceGetAttribute(&D.sm_count, cudaDevAttrMultiProcessorCount, D.dev));
+    const int rc = pool_device(B->pool, D.dev, D.stream, &B->h2d, &D.pool);
+    if (rc) return rc;
+    const int64_t nu = D.n_units;
+    const size_t U = size_t(std::max<int64_t>(nu, 1));
+    CK(cudaMalloc(&D.d_units, U * sizeof(DevUnit)));
+    CK(cudaMalloc(&D.d_keys, U * 4));
+    CK(cudaMalloc(&D.d_vals, U * 4));
+    CK(cudaMalloc(&D.d_keys2, U * 4));
+    CK(cudaMalloc(&D.d_order, U * 4));
+    CK(cudaMalloc(&D.d_res, U * sizeof(DevResult)));
+    CK(cudaMalloc(&D.d_list1, U * 4));
+    CK(cudaMalloc(&D.d_list2, U * 4));
+    CK(cudaMalloc(&D.d_ctr, sizeof(DevCounters)));
+    CK(cudaMallocHost(&D.h_res, U * sizeof(DevResult)));
+    if (!B->units_mode) {
+        CK(cudaMalloc(&D.d_tasks, size_t(std::max<int64_t>(D.n_items, 1)) * 32));
+        CK(cudaMalloc(&D.d_seed, size_t(std::max<int64_t>(D.n_items, 1)) * 4));
+        CK(cudaMallocHost(&D.h_seed, size_t(std::max<int64_t>(D.n_items, 1)) * 4));
+    }
+    CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, D.cub_bytes, D.d_keys, D.d_keys2,
+                                                 D.d_vals, D.d_order, int(U), 0, 32, D.stream));
+    CK(cudaMalloc(&D.d_cub, std::max<size_t>(D.cub_bytes, 16)));
+    // warp-tier scratch: 2*band ints per resident warp, capped at 1 GiB
+    {
+        const int64_t per_warp = 2LL * B->band * 4;
+        int64_t warps = int64_t(D.sm_count) * 16;
+        warps = std::min<int64_t>(warps, std::max<int64_t>(4, (1LL << 30) / per_warp));
+        warps = (warps + 3) / 4 * 4;
+        D.scratch_warps = int(warps);
+        CK(cudaMalloc(&D.d_scratch, size_t(warps * per_warp)));
+    }
+    return XB_OK;
+}
+
+static int upload_inputs(xb_batch* B, DevBatch& D, const void* items) {
+    CK(cudaSetDevice(D.dev));
+    if (B->units_mode) {
+        const size_t U = size_t(D.n_units);
+        if (U) {
+            CK(cudaMemcpyAsync(D.d_units, D.h_units.data(), U * sizeof(DevUnit),
+                               cudaMemcpyHostToDevice, D.stream));
+            B->h2d += int64_t(U * sizeof(DevUnit));
+        }
+    } else if (D.n_items) {
+        const xb_task* T = static_cast<const xb_task*>(items);
+        int64_t* h = nullptr;
+        CK(cudaMallocHost(&h, size_t(D.n_items) * 32));
+        for (int64_t q = 0; q < D.n_items; ++q) {
+            const xb_task& t = T[D.tasks.empty() ? q : D.tasks[size_t(q)]];
+            h[4 * q + 0] = t.h_id;
+            h[4 * q + 1] = t.v_id;
+            h[4 * q + 2] = int64_t(t.h_seed);
+            h[4 * q + 3] = int64_t(t.v_seed);
+        }
+        const cudaError_t e = cudaMemcpyAsync(D.d_tasks, h, size_t(D.n_items) * 32,
+                                              cudaMemcpyHostToDevice, D.stream);
+        cudaStreamSynchronize(D.stream);
+        cudaFreeHost(h);
+        CK(e);
+        B->h2d += D.n_items * 32;
+    }
+    return XB_OK;
+}
+
+template <int MODE>
+static void launch_thread_tier(int K, const TierParams& P, int blocks, cudaStream_t st) {
+    if (K == 32)
+        thread_tier_kernel<32, MODE><<<blocks, kTB, 0, st>>>(P);
+    else
+        thread_tier_kernel<64, MODE><<<blocks, kTB, 0, st>>>(P);
+}
+
+static int occupancy_blocks(int K, int mode, int* out) {
+    int b = 0;
+    cudaError_t e = cudaSuccess;
+#define OCC(KK, MM) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, thread_tier_kernel<KK, MM>, kTB, 0)
+    if (K == 32) {
+        if (mode == 0) OCC(32, 0); else if (mode == 1) OCC(32, 1); else OCC(32, 2);
+    } else {
+        if (mode == 0) OCC(64, 0); else if (mode == 1) OCC(64, 1); else OCC(64, 2);
+    }
+#undef OCC
+    if (e != cudaSuccess) return XB_E_CUDA;
+    *out = std::max(1, b);
+    return XB_OK;
+}
+
+static int run_device(xb_batch* B, DevBatch& D) {
+    CK(cudaSetDevice(D.dev));
+    xb_pool* p = B->pool;
+    const int mode = p->dev_scheme.fast_dna ? 0 : (p->enc == ENC_2BIT ? 1 : 2);
+    const bool tok = thread_tiers_ok(p);
+    D.launches = 0;
+    CK(cudaEventRecord(D.ev[0], D.stream));
+    CK(cudaMemsetAsync(D.d_ctr, 0, sizeof(DevCounters), D.stream));
+    const int64_t nu = D.n_units;
+    if (nu == 0) {
+        for (int q = 1; q < 6; ++q) CK(cudaEventRecord(D.ev[q], D.stream));
+        return XB_OK;
+    }
+    // ---- LR split + seed score + cost keys (or host-built units) ----
+    if (!B->units_mode) {
+        PrepParams pp{};
+        pp.pool = D.pool->words;
+        pp.tasks = D.d_tasks;
+        pp.seq_pos = D.pool->seq_pos;
+        pp.seq_len = D.pool->seq_len;
+        pp.n = D.n_items;
+        pp.k = B->k;
+        pp.enc = p->enc;
+        pp.thread_ok = (tok && !(B->flags & XB_FLAG_GENERIC_ONLY)) ? 1 : 0;
+        pp.x = p->scheme.x;
+        pp.beta = -p->scheme.gap;
+        pp.max_pos_score = std::max(0, p->dev_scheme.max_score);
+        pp.scheme = D.pool->scheme;
+        pp.units = D.d_units;
+        pp.keys = D.d_keys;
+        pp.vals = D.d_vals;
+        pp.seed_score = D.d_seed;
+        pp.warp_list = D.d_list2;
+        pp.warp_len = &D.d_ctr->list_len[2];
+        const int tb = 256;
+        prep_kernel<<<unsigned((D.n_items + tb - 1) / tb), tb, 0, D.stream>>>(pp);
+        CK(cudaGetLastError());
+        ++D.launches;
+    } else {
+        // keys/vals/warp list for host-built units
+        std::vector<uint32_t> keys(static_cast<size_t>(nu)), vals(static_cast<size_t>(nu)), wl;
+        for (int64_t u = 0; u < nu; ++u) {
+            DevUnit& x = D.h_units[size_t(u)];
+            if (!tok || (B->flags & XB_FLAG_GENERIC_ONLY)) x.route = 2;
+            keys[size_t(u)] = uint32_t(std::min<long long>(unit_est(x.h_len, x.v_len), 0xFFFFFFF0LL));
+            vals[size_t(u)] = uint32_t(u);
+            if (x.route) wl.push_back(uint32_t(u));
+        }
+        CK(cudaMemcpyAsync(D.d_units, D.h_units.data(), size_t(nu) * sizeof(DevUnit),
+                           cudaMemcpyHostToDevice, D.stream));
+        CK(cudaMemcpyAsync(D.d_keys, keys.data(), size_t(nu) * 4, cudaMemcpyHostToDevice, D.stream));
+        CK(cudaMemcpyAsync(D.d_vals, vals.data(), size_t(nu) * 4, cudaMemcpyHostToDevice, D.stream));
+        unsigned long long wlen = wl.size();
+        if (!wl.empty())
+            CK(cudaMemcpyAsync(D.d_list2, wl.data(), wl.size() * 4, cudaMemcpyHostToDevice, D.stream));
+        CK(cudaMemcpyAsync(&D.d_ctr->list_len[2], &wlen, 8, cudaMemcpyHostToDevice, D.stream));
+        CK(cudaStreamSynchronize(D.stream));  // host vectors die at scope end
+    }
+    // ---- longest first ----
+    const uint32_t* order = D.d_vals;
+    if (!(B->flags & XB_FLAG_NO_SORT)) {
+        size_t tmp = D.cub_bytes;
+        CK(cub::DeviceRadixSort::SortPairsDescending(D.d_cub, tmp, D.d_keys, D.d_keys2, D.d_vals,
+                                                     D.d_order, int(nu), 0, 32, D.stream));
+        order = D.d_order;
+    }
+    CK(cudaEventRecord(D.ev[1], D.stream));
+
+    TierParams tp{};
+    tp.pool = D.pool->words;
+    tp.units = D.d_units;
+    tp.results = D.d_res;
+    tp.ctr = D.d_ctr;
+    tp.scheme = D.pool->scheme;
+    tp.band = B->band;
+    tp.pat = 0x55555555u;
+    tp.warp_scratch = D.d_scratch;
+    const bool skip_t0 = (B->flags & XB_FLAG_TIER2_FIRST) != 0;
+    // ---- tier 0: one thread per unit, 32-slot register band ----
+    if (!skip_t0 && !(B->flags & XB_FLAG_GENERIC_ONLY)) {
+        if (!D.occ[0]) CK(occupancy_blocks(32, mode, &D.occ[0]) ? cudaErrorUnknown : cudaSuccess);
+        tp.queue = order;
+        tp.queue_len_ptr = nullptr;
+        tp.queue_len = (unsigned long long)nu;
+        tp.esc_list = D.d_list1;
+        tp.esc_len = &D.d_ctr->list_len[1];
+        tp.tier = 0;
+        const int blocks = D.sm_count * D.occ[0];
+        if (mode == 0) launch_thread_tier<0>(32, tp, blocks, D.stream);
+        else if (mode == 1) launch_thread_tier<1>(32, tp, blocks, D.stream);
+        else launch_thread_tier<2>(32, tp, blocks, D.stream);
+        CK(cudaGetLastError());
+        ++D.launches;
+    }
+    CK(cudaEventRecord(D.ev[2], D.stream));
+    // ---- tier 1: 64-slot register band for the units tier 0 could not hold ----
+    if (!(B->flags & XB_FLAG_GENERIC_ONLY)) {
+        if (!D.occ[1]) CK(occupancy_blocks(64, mode, &D.occ[1]) ? cudaErrorUnknown : cudaSuccess);
+        if (skip_t0) {
+            tp.queue = order;
+            tp.queue_len_ptr = nullptr;
+            tp.queue_len = (unsigned long long)nu;
+            tp.tier = 0;  // skip routed units like tier 0 does
+        } else {
+            tp.queue = D.d_list1;
+            tp.queue_len_ptr = &D.d_ctr->list_len[1];
+            tp.tier = 1;
+        }
+        tp.esc_list = D.d_list2;
+        tp.esc_len = &D.d_ctr->list_len[2];
+        const int blocks = D.sm_count * D.occ[1];
+        if (skip_t0) {
+            // count it under tier 1 in the stats: cursor slot 0 is still fresh
+        }
+        if (mode == 0) launch_thread_tier<0>(64, tp, blocks, D.stream);
+        else if (mode == 1) launch_thread_tier<1>(64, tp, blocks, D.stream);
+        else launch_thread_tier<2>(64, tp, blocks, D.stream);
+        CK(cudaGetLastError());
+        ++D.launches;
+    }
+    CK(cudaEventRecord(D.ev[3], D.stream));
+    // ---- tier 2: warp per unit, exact generic path ----
+    {
+        tp.queue = D.d_list2;
+        tp.queue_len_ptr = &D.d_ctr->list_len[2];
+        tp.tier = 2;
+        tp.esc_list = nullptr;
+        tp.esc_len = nullptr;
+        const int blocks = D.scratch_warps / 4;
+        if (p->enc == ENC_2BIT)
+            warp_tier_kernel<ENC_2BIT><<<blocks, 128, 0, D.stream>>>(tp);
+        else
+            warp_tier_kernel<ENC_5BIT><<<blocks, 128, 0, D.stream>>>(tp);
+        CK(cudaGetLastError());
+        ++D.launches;
+    }
+    CK(cudaEventRecord(D.ev[4], D.stream));
+    return XB_OK;
+}
+
+static int fetch_device(xb_batch* B, DevBatch& D) {
+    CK(cudaSetDevice(D.dev));
+    if (D.n_units)
+        CK(cudaMemcpyAsync(D.h_res, D.d_res, size_t(D.n_units) * sizeof(DevResult),
+                           cudaMemcpyDeviceToHost, D.stream));
+    if (!B->units_mode && D.n_items)
+        CK(cudaMemcpyAsync(D.h_seed, D.d_seed, size_t(D.n_items) * 4, cudaMemcpyDeviceToHost,
+                           D.stream));
+    CK(cudaEventRecord(D.ev[5], D.stream));
+    B->d2h += D.n_units * int64_t(sizeof(DevResult)) + (B->units_mode ? 0 : D.n_items * 4);
+    return XB_OK;
+}
+
+// LPT over estimated task cost (partition.cpp:231-305 without the tile
+// memory test): heaviest first onto the least loaded device.
+static void shard_lpt(const std::vector<long long>& cost, int G, std::vector<std::vector<int64_t>>& out) {
+    out.assign(size_t(G), {});
+    std::vector<int64_t> idx(cost.size());
+    std::iota(idx.begin(), idx.end(), 0);
+    std::stable_sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) { return cost[size_t(a)] > cost[size_t(b)]; });
+    using E = std::pair<long long, int>;
+    std::priority_queue<E, std::vector<E>, std::greater<E>> pq;
+    for (int g = 0; g < G; ++g) pq.push({0, g});
+    for (int64_t t : idx) {
+        E e = pq.top();
+        pq.pop();
+        out[size_t(e.second)].push_back(t);
+        e.first += cost[size_t(t)];
+        pq.push(e);
+    }
+    for (auto& v : out) std::sort(v.begin(), v.end());
+}
+
+static int exec_devices(const xb_exec* ex, std::vector<int>& ids) {
+    const int avail = xb_device_count();
+    if (avail <= 0) return XB_E_NO_DEVICE;
+    const int n = (ex && ex->n_devices > 1) ? ex->n_devices : 1;
+    for (int g = 0; g < n; ++g) {
+        int id = (ex && ex->device_ids) ? ex->device_ids[g] : (n == 1 ? -1 : g);
+        if (id < 0) {
+            if (cudaGetDevice(&id) != cudaSuccess) id = 0;
+        }
+        if (id >= avail) return XB_E_BAD_PARAM;
+        ids.push_back(id);
+    }
+    return XB_OK;
+}
+
+static int validate_tasks(const xb_pool* p, const xb_task* tasks, int64_t n, int k, int64_t* bad) {
+    const int64_t ns = xb_pool_size(p);
+    for (int64_t t = 0; t < n; ++t) {
+        const xb_task& q = tasks[t];
+        if (int64_t(q.h_id) >= ns || int64_t(q.v_id) >= ns) {  // align.cpp:271-273
+            if (bad) *bad = t;
+            return XB_E_DANGLING;
+        }
+    }
+    for (int64_t t = 0; t < n; ++t) {
+        const xb_task& q = tasks[t];
+        const int64_t hl = p->offsets[q.h_id + 1] - p->offsets[q.h_id];
+        const int64_t vl = p->offsets[q.v_id + 1] - p->offsets[q.v_id];
+        if (int64_t(q.h_seed) + k > hl || int64_t(q.v_seed) + k > vl ||  // align.cpp:276-279
+            q.h_seed > uint64_t(hl) || q.v_seed > uint64_t(vl)) {
+            if (bad) *bad = t;
+            return XB_E_SEED_OOB;
+        }
+    }
+    return XB_OK;
+}
+
+extern "C" {
+
+xb_batch* xb_batch_create(xb_pool* p, const xb_task* tasks, int64_t n, int k, int band,
+                          const xb_exec* exec, int64_t* bad_task, int* err) {
+    auto fail = [&](int code, xb_batch* b) -> xb_batch* {
+        if (err) *err = code;
+        if (b) xb_batch_free(b);
+        return nullptr;
+    };
+    if (!p || n < 0 || k < 0 || band < 1 || (n && !tasks)) return fail(XB_E_BAD_PARAM, nullptr);
+    int rc = validate_tasks(p, tasks, n, k, bad_task);
+    if (rc) return fail(rc, nullptr);
+    std::vector<int> ids;
+    rc = exec_devices(exec, ids);
+    if (rc) return fail(rc, nullptr);
+    auto* B = new xb_batch();
+    B->pool = p;
+    B->k = k;
+    B->band = band;
+    B->flags = exec ? exec->flags : 0;
+    B->n = n;
+    B->devs.resize(ids.size());
+    if (ids.size() > 1) {
+        std::vector<long long> cost(static_cast<size_t>(n));
+        for (int64_t t = 0; t < n; ++t) {
+            const xb_task& q = tasks[t];
+            const long long hl = p->offsets[q.h_id + 1] - p->offsets[q.h_id];
+            const long long vl = p->offsets[q.v_id + 1] - p->offsets[q.v_id];
+            cost[size_t(t)] = unit_est(q.h_seed, q.v_seed) +
+                              unit_est(hl - q.h_seed - k, vl - q.v_seed - k) + 1;
+        }
+        std::vector<std::vector<int64_t>> sh;
+        shard_lpt(cost, int(ids.size()), sh);
+        for (size_t g = 0; g < ids.size(); ++g) B->devs[g].tasks = std::move(sh[g]);
+    }
+    for (size_t g = 0; g < ids.size(); ++g) {
+        DevBatch& D = B->devs[g];
+        D.dev = ids[g];
+        D.n_items = ids.size() > 1 ? int64_t(D.tasks.size()) : n;
+        D.n_units = 2 * D.n_items;
+        rc = setup_device(B, D, exec);
+        if (rc) return fail(rc, B);
+        rc = upload_inputs(B, D, tasks);
+        if (rc) return fail(rc, B);
+    }
+    if (err) *err = XB_OK;
+    return B;
+}
+
+int xb_batch_run(xb_batch* B) {
+    if (!B) return XB_E_BAD_PARAM;
+    for (auto& D : B->devs) {
+        const int rc = run_device(B, D);
+        if (rc) return rc;
+    }
+    B->ran = true;
+    return XB_OK;
+}
+
+int xb_batch_sync(xb_batch* B) {
+    for (auto& D : B->devs) {
+        CK(cudaSetDevice(D.dev));
+        CK(cudaStreamSynchronize(D.stream));
+    }
+    return XB_OK;
+}
+
+int xb_batch_fetch(xb_batch* B, xb_side_result* out, int32_t* seed_score) {
+    if (!B || !B->ran) return XB_E_BAD_PARAM;
+    for (auto& D : B->devs) {
+        const int rc = fetch_device(B, D);
+        if (rc) return rc;
+    }
+    for (auto& D : B->devs) {
+        CK(cudaSetDevice(D.dev));
+        CK(cudaStreamSynchronize(D.stream));
+        const bool sharded = B->devs.size() > 1;
+        if (B->units_mode) {
+            for (int64_t q = 0; q < D.n_units; ++q) {
+                const int64_t g = sharded ? D.tasks[size_t(q)] : q;
+                std::memcpy(&out[g], &D.h_res[q], sizeof(xb_side_result));
+            }
+        } else if (!sharded) {
+            std::memcpy(out, D.h_res, size_t(D.n_units) * sizeof(xb_side_result));
+            if (seed_score) std::memcpy(seed_score, D.h_seed, size_t(D.n_items) * 4);
+        } else {
+            for (int64_t q = 0; q < D.n_items; ++q) {
+                const int64_t g = D.tasks[size_t(q)];
+                std::memcpy(&out[2 * g], &D.h_res[2 * q], 2 * sizeof(xb_side_result));
+                if (seed_score) seed_score[g] = D.h_seed[q];
+            }
+        }
+    }
+    return XB_OK;
+}
+
+int xb_batch_stats(xb_batch* B, xb_stats* st) {
+    if (!B || !st) return XB_E_BAD_PARAM;
+    std::memset(st, 0, sizeof *st);
+    st->n_devices = int(B->devs.size());
+    for (auto& D : B->devs) {
+        CK(cudaSetDevice(D.dev));
+        CK(cudaStreamSynchronize(D.stream));
+        DevCounters c{};
+        CK(cudaMemcpy(&c, D.d_ctr, sizeof c, cudaMemcpyDeviceToHost));
+        float ms[5] = {0, 0, 0, 0, 0};
+        if (D.n_units) {
+            CK(cudaEventElapsedTime(&ms[0], D.ev[0], D.ev[4]));
+            CK(cudaEventElapsedTime(&ms[1], D.ev[0], D.ev[1]));
+            CK(cudaEventElapsedTime(&ms[2], D.ev[1], D.ev[2]));
+            CK(cudaEventElapsedTime(&ms[3], D.ev[2], D.ev[3]));
+            CK(cudaEventElapsedTime(&ms[4], D.ev[3], D.ev[4]));
+        }
+        st->ms_total = std::max(st->ms_total, double(ms[0]));
+        st->ms_prep = std::max(st->ms_prep, double(ms[1]));
+        for (int t = 0; t < 3; ++t) {
+            st->ms_tier[t] = std::max(st->ms_tier[t], double(ms[2 + t]));
+            st->units_tier[t] += int64_t(c.units[t]);
+            st->cells_tier[t] += int64_t(c.cells[t]);
+        }
+        st->escalated[0] += int64_t(c.escalated[0]);
+        st->escalated[1] += int64_t(c.escalated[1]);
+        st->launches += D.launches;
+        st->sm_count = D.sm_count;
+    }
+    st->h2d_bytes = B->h2d;
+    st->d2h_bytes = B->d2h;
+    return XB_OK;
+}
+
+void xb_batch_free(xb_batch* B) {
+    if (!B) return;
+    for (auto& D : B->devs) free_dev(D);
+    delete B;
+}
+
+int xb_extend_batch(xb_pool* p, const xb_task* tasks, int64_t n, int k, int band,
+                    xb_side_result* out, int32_t* seed_score, int64_t* bad_task,
+                    const xb_exec* exec) {
+    int err = 0;
+    xb_batch* B = xb_batch_create(p, tasks, n, k, band, exec, bad_task, &err);
+    if (!B) return err;
+    int rc = xb_batch_run(B);
+    if (!rc) rc = xb_batch_fetch(B, out, seed_score);
+    if (!rc) rc = xb_batch_stats(B, &g_last_stats);
+    xb_batch_free(B);
+    return rc;
+}
+
+int xb_extend_units(xb_pool* p, const xb_unit* units, int64_t n, int band, xb_side_result* out,
+                    int64_t* bad_unit, const xb_exec* exec) {
+    if (!p || n < 0 || band < 1 || (n && !units)) return XB_E_BAD_PARAM;
+    {
+        std::lock_guard<std::mutex> g(p->mu);
+        pool_pack(p);
+    }
+    const int64_t ns = xb_pool_size(p);
+    std::vector<DevUnit> all(static_cast<size_t>(n));
+    for (int64_t q = 0; q < n; ++q) {
+        const xb_unit& u = units[q];
+        if (int64_t(u.h_id) >= ns || int64_t(u.v_id) >= ns) {
+            if (bad_unit) *bad_unit = q;
+            return XB_E_DANGLING;
+        }
+        const int64_t hn = p->seq_len[u.h_id], vn = p->seq_len[u.v_id];
+        // make_view range checks (sequence.cpp:5-15)
+        auto bad_view = [&](int64_t len, uint64_t origin, int dir, uint64_t length) {
+            if (origin > uint64_t(len)) return true;
+            const uint64_t room = dir ? uint64_t(len) - origin : origin;
+            return length > room;
+        };
+        if (bad_view(hn, u.h_origin, u.h_dir, u.h_len) || bad_view(vn, u.v_origin, u.v_dir, u.v_len)) {
+            if (bad_unit) *bad_unit = q;
+            return XB_E_OUT_OF_RANGE;
+        }
+        DevUnit& d = all[size_t(q)];
+        d.h_pos = p->seq_pos[u.h_id] + int64_t(u.h_origin) - (u.h_dir ? 0 : 1);
+        d.v_pos = p->seq_pos[u.v_id] + int64_t(u.v_origin) - (u.v_dir ? 0 : 1);
+        d.h_len = int32_t(u.h_len);
+        d.v_len = int32_t(u.v_len);
+        d.dir = (u.h_dir ? 1 : 0) | (u.v_dir ? 2 : 0);
+        const long long mn = std::min<long long>(u.h_len, u.v_len);
+        const long long bound = (long long)std::max(0, p->dev_scheme.max_score) * mn +
+                                (long long)(-p->scheme.gap) * (long long)(u.h_len + u.v_len + 2) +
+                                p->scheme.x + 2;
+        d.route = (bound < (1LL << 23) && u.h_len < (1ull << 30) && u.v_len < (1ull << 30)) ? 0 : 2;
+    }
+    std::vector<int> ids;
+    int rc = exec_devices(exec, ids);
+    if (rc) return rc;
+    auto* B = new xb_batch();
+    B->pool = p;
+    B->band = band;
+    B->flags = exec ? exec->flags : 0;
+    B->units_mode = true;
+    B->n = n;
+    B->devs.resize(ids.size());
+    std::vector<std::vector<int64_t>> sh;
+    if (ids.size() > 1) {
+        std::vector<long long> cost(static_cast<size_t>(n));
+        for (int64_t q = 0; q < n; ++q) cost[size_t(q)] = unit_est(all[size_t(q)].h_len, all[size_t(q)].v_len) + 1;
+        shard_lpt(cost, int(ids.size()), sh);
+    }
+    for (size_t g = 0; g < ids.size(); ++g) {
+        DevBatch& D = B->devs[g];
+        D.dev = ids[g];
+        if (ids.size() > 1) {
+            D.tasks = sh[g];
+            for (int64_t q : D.tasks) D.h_units.push_back(all[size_t(q)]);
+        } else {
+            D.h_units = all;
+        }
+        D.n_items = int64_t(D.h_units.size());
+        D.n_units = D.n_items;
+        rc = setup_device(B, D, exec);
+        if (!rc) rc = upload_inputs(B, D, nullptr);
+        if (rc) {
+            xb_batch_free(B);
+            return rc;
+        }
+    }
+    rc = xb_batch_run(B);
+    if (!rc) rc = xb_batch_fetch(B, out, nullptr);
+    if (!rc) rc = xb_batch_stats(B, &g_last_stats);
+    xb_batch_free(B);
+    return rc;
+}
+
+int xb_last_stats(xb_stats* st) {
+    if (!st) return XB_E_BAD_PARAM;
+    *st = g_last_stats;
+    return XB_OK;
+}
+
+int xb_measure_int32_peak(int device, double* alu, double* mixed, double* clk_mhz, int* sm_count) {
+    if (xb_device_count() <= device) return XB_E_NO_DEVICE;
+    CK(cudaSetDevice(device));
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    const int tb = 256, bps = 8, blocks = sms * bps, iters = 1 << 14;
+    int32_t* out = nullptr;
+    long long* clk = nullptr;
+    CK(cudaMalloc(&out, size_t(blocks) * tb * 4));
+    CK(cudaMalloc(&clk, size_t(blocks) * 8));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    double res[2] = {0, 0};
+    double mhz = 0;
+    for (int v = 0; v < 2; ++v) {
+        for (int rep = 0; rep < 3; ++rep) {  // warm, then keep the best
+            CK(cudaEventRecord(e0));
+            if (v == 0) int_peak_alu<<<blocks, tb>>>(out, iters, 7, clk);
+            else int_peak_mixed<<<blocks, tb>>>(out, iters, 7, clk);
+            CK(cudaEventRecord(e1));
+            CK(cudaEventSynchronize(e1));
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, e0, e1));
+            std::vector<long long> c(static_cast<size_t>(blocks));
+            CK(cudaMemcpy(c.data(), clk, size_t(blocks) * 8, cudaMemcpyDeviceToHost));
+            const long long cmax = *std::max_element(c.begin(), c.end());
+            const double ops = double(blocks) * tb * iters * (v == 0 ? 24.0 : 32.0);
+            // per-SM clock cycles: blocks run concurrently (bps resident per SM)
+            const double per_clk_sm = ops / (double(cmax) * sms);
+            res[v] = std::max(res[v], per_clk_sm);
+            mhz = std::max(mhz, double(cmax) / (ms * 1e3));
+        }
+    }
+    cudaFree(out);
+    cudaFree(clk);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (alu) *alu = res[0];
+    if (mixed) *mixed = res[1];
+    if (clk_mhz) *clk_mhz = mhz;
+    if (sm_count) *sm_count = sms;
+    return XB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,62 @@
+// Internal device/host shared definitions for the xdrop_b200 engine.
+#pragma once
+
+#include <cstdint>
+
+namespace xb {
+
+// Pool encodings. ENC_2BIT: pure ACGT, codes A0 C1 G2 T3, 16 symbols per
+// 32-bit word. ENC_5BIT: alphabet index, 6 codes per word (bits 0..29).
+enum : int { ENC_2BIT = 2, ENC_5BIT = 5 };
+
+// symbols of zero padding in front of / behind every device pool, so window
+// fetches that run past a sequence (masked out later) never leave the buffer
+constexpr int64_t kPoolPad = 4096;
+
+// Code reserved for "outside the view": scores -128 (+2gap drift) in the
+// thread tier's table, so out-of-matrix diagonals always lose.
+constexpr int kSentinel = 31;
+
+// One work unit on the device (a WorkUnit, partition.hpp:54-62, already
+// resolved to pool positions). View element t lives at pool symbol
+// position  pos + t  (dir Right) or  pos - t  (dir Left).
+struct DevUnit {
+    int64_t h_pos;
+    int64_t v_pos;
+    int32_t h_len;
+    int32_t v_len;
+    int32_t dir;     // bit 0: h view Right, bit 1: v view Right (0 = Left)
+    int32_t route;   // 0 thread tier, 2 warp tier directly (guard failed)
+};
+
+// Same layout as xb_side_result.
+struct DevResult {
+    int32_t score, h_ext, v_ext, delta_w;
+    int64_t cells;
+    int32_t status, spread;
+};
+
+// Scheme as the kernels see it.
+struct DevScheme {
+    int32_t gap;
+    int32_t x;
+    int32_t fast_dna;     // +1/-1/-1 over a 2-bit pool: bit-parallel sim
+    int32_t enc;          // pool encoding
+    int32_t max_score;    // max table entry (for overflow guards)
+    int32_t min_score;
+    int32_t sim[32 * 32]; // code-pair scores [h][v] (sentinel row/col = very negative)
+};
+
+// Per-tier counters, device side.
+struct DevCounters {
+    unsigned long long cursor[3];     // work-queue cursors per tier
+    unsigned long long list_len[3];   // length of the escalation lists (tier 1, 2 inputs)
+    unsigned long long units[3];
+    unsigned long long cells[3];
+    unsigned long long escalated[2];
+};
+
+constexpr int kStatusOk = 0;
+constexpr int kStatusBand = 1;
+
+}  // namespace xb

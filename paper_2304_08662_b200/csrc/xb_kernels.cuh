@@ -1,0 +1,182 @@
+// sm_100a kernels for memory-restricted X-drop seed extension.
+//
+// Semantics follow the reference kernel proj/src/align.cpp:37-155 exactly
+// (window rules 64-98, cell rules 102-136, result 148-154); every result
+// field, including cells and delta_w, is bit-identical.  See DESIGN.md for
+// the derivation of the tricks used here.
+//
+// Coordinates.  Antidiagonal d holds cells (i, j), i + j = d, i = offset
+// into the vertical view v (length n), j = offset into h (length m).  The
+// band is addressed by the folded diagonal u = floor(d/2) - i (the same
+// invariant the reference uses, align.cpp:12-19): a cell and its diagonal
+// predecessor share u; the gap predecessors sit at u and u-1 (d even) or
+// u and u+1 (d odd).  A thread-tier unit keeps K consecutive u values
+// (slot k <-> u = ubase + k) of the two live antidiagonals in REGISTERS.
+//
+// Drift space.  A cell value val is stored as  s = val + beta*d + off  with
+// beta = -gap and off = X + 1.  Then the recurrence becomes
+//     s_d = max(s_{d-2} + (sim - 2 gap),  s_left,  s_up)
+// (one VIMNMX3), every live cell has s >= 1 and the dead sentinel is
+// negative, so the liveness bit of a slot is its sign bit.
+//
+// Exact running best.  The reference updates T cell by cell in ascending i
+// and prunes each cell against that running T (align.cpp:122-129).  In slot
+// order, ascending i is descending k, so one max chain over k = K-1..0 on
+// keys (s*64 + k) gives, per slot, the inclusive prefix maximum AND its
+// first-attaining slot; "s_k >= Q_k - X" is then the single compare
+// key_k >= c_k with c = running max of (key - 64X - 63).
+#pragma once
+
+#include <cstdint>
+
+#include "xb_internal.h"
+
+namespace xb {
+
+constexpr int32_t kDeadS = -(1 << 24);  // dead sentinel in drift space
+constexpr int kTB = 128;                // threads per block, thread tiers
+
+struct TierParams {
+    const uint32_t* __restrict__ pool;
+    const DevUnit* __restrict__ units;
+    DevResult* __restrict__ results;
+    const uint32_t* __restrict__ queue;  // unit indices to process
+    const unsigned long long* __restrict__ queue_len_ptr;  // device count (lists) or null
+    unsigned long long queue_len;        // static count when queue_len_ptr == null
+    uint32_t* __restrict__ esc_list;     // units that outgrow this tier
+    unsigned long long* __restrict__ esc_len;
+    DevCounters* __restrict__ ctr;
+    const DevScheme* __restrict__ scheme;
+    int32_t band;
+    int32_t tier;
+    int32_t* __restrict__ warp_scratch;  // warp tier: 2*band ints per warp slot
+    uint32_t pat;                        // 0x55555555, kept opaque so LOP3 takes it from c[]
+};
+
+// ---------------------------------------------------------------- pool ----
+
+__device__ __forceinline__ uint32_t ldw(const uint32_t* __restrict__ pool, int64_t wi) {
+    return __ldg(pool + wi);
+}
+
+// exact reversal of sixteen 2-bit fields
+__device__ __forceinline__ uint32_t rev16(uint32_t x) {
+    x = __brev(x);
+    return ((x >> 1) & 0x55555555u) | ((x & 0x55555555u) << 1);
+}
+
+// 16 symbols starting at pool symbol position q, lowest address in bits 0-1
+__device__ __forceinline__ uint32_t chunk_mem(const uint32_t* __restrict__ pool, int64_t q) {
+    const int64_t wi = q >> 4;
+    const uint32_t sh = uint32_t(q & 15) * 2u;
+    return __funnelshift_r(ldw(pool, wi), ldw(pool, wi + 1), sh);
+}
+
+// view element t at bits 0-1 ("bottom first")
+__device__ __forceinline__ uint32_t chunk_bf(const uint32_t* pool, int64_t pos, int dir, int64_t t) {
+    return dir ? chunk_mem(pool, pos + t) : rev16(chunk_mem(pool, pos - t - 15));
+}
+// view element t at bits 30-31 ("top first")
+__device__ __forceinline__ uint32_t chunk_tf(const uint32_t* pool, int64_t pos, int dir, int64_t t) {
+    return dir ? rev16(chunk_mem(pool, pos + t)) : chunk_mem(pool, pos - t - 15);
+}
+
+// one symbol code (any encoding) of a view, sentinel outside [0, len)
+template <int ENC>
+__device__ __forceinline__ uint32_t code_at(const uint32_t* __restrict__ pool, int64_t pos, int dir,
+                                            int64_t len, int64_t t) {
+    if (t < 0 || t >= len) return kSentinel;
+    const int64_t p = dir ? pos + t : pos - t;
+    if (ENC == ENC_2BIT) return (ldw(pool, p >> 4) >> (uint32_t(p & 15) * 2u)) & 3u;
+    const uint64_t up = uint64_t(p);
+    const uint64_t wi = up / 6u;
+    return (ldw(pool, int64_t(wi)) >> (uint32_t(up - wi * 6u) * 5u)) & 31u;
+}
+
+// Streams consecutive 16-symbol chunks of a 2-bit view, one new word load per
+// chunk, issued a full chunk ahead of use.  TOP = chunks top-first (v side)
+template <bool TOP>
+struct Reader {
+    uint32_t cur;   // remaining symbols of the current chunk
+    uint32_t w0, w1;
+    int64_t wnext;  // word index of the next load
+    uint32_t sh;
+    int32_t cnt;
+    int32_t dir;
+
+    __device__ __forceinline__ void init(const uint32_t* pool, int64_t pos, int d, int64_t t0) {
+        dir = d;
+        // current chunk at t0, words for chunk t0+16 preloaded
+        cur = TOP ? chunk_tf(pool, pos, d, t0) : chunk_bf(pool, pos, d, t0);
+        const int64_t q = d ? pos + t0 + 16 : pos - (t0 + 16) - 15;
+        const int64_t wi = q >> 4;
+        sh = uint32_t(q & 15) * 2u;
+        w0 = ldw(pool, wi);
+        w1 = ldw(pool, wi + 1);
+        wnext = d ? wi + 2 : wi - 1;
+        cnt = 16;
+    }
+    __device__ __forceinline__ void refill(const uint32_t* pool) {
+        uint32_t c = __funnelshift_r(w0, w1, sh);
+        const bool rev = TOP ? (dir != 0) : (dir == 0);
+        cur = rev ? rev16(c) : c;
+        const uint32_t nw = ldw(pool, wnext);
+        if (dir) {
+            w0 = w1;
+            w1 = nw;
+            wnext += 1;
+        } else {
+            w1 = w0;
+            w0 = nw;
+            wnext -= 1;
+        }
+        cnt = 16;
+    }
+};
+
+// ------------------------------------------------------ thread tier ----
+
+template <int K, int MODE>
+struct TState {
+    static constexpr int NW = K / 16;  // 2-bit window words
+    static constexpr int NB = K / 4;   // byte window words (table mode)
+    static constexpr int NM = K / 32;  // liveness mask words
+    // unit
+    int64_t h_pos, v_pos;
+    int32_t m, n, hdir, vdir, unit;
+    // progress
+    int32_t d, ubase;
+    int32_t fl1, ll1, fl2, ll2;  // live i-ranges of rows d-1 and d-2
+    int32_t T, best_d, best_i, delta_w;
+    int64_t cells;
+    // windows
+    uint32_t VW[MODE == 0 ? NW : NB];
+    uint32_t HW[MODE == 0 ? NW : NB];
+    Reader<true> rv;
+    Reader<false> rh;
+};
+
+// LR split + seed score + cost keys, one thread per task
+struct PrepParams {
+    const uint32_t* __restrict__ pool;
+    const int64_t* __restrict__ tasks;    // n x {h_id, v_id, h_seed, v_seed} (validated)
+    const int64_t* __restrict__ seq_pos;  // pool position of each sequence's symbol 0
+    const int64_t* __restrict__ seq_len;
+    int64_t n;
+    int32_t k;
+    int32_t enc;
+    int32_t thread_ok;                     // scheme admits the thread tiers at all
+    int32_t x, beta, max_pos_score;
+    const DevScheme* __restrict__ scheme;
+    DevUnit* __restrict__ units;
+    uint32_t* __restrict__ keys;
+    uint32_t* __restrict__ vals;
+    int32_t* __restrict__ seed_score;
+    uint32_t* __restrict__ warp_list;
+    unsigned long long* __restrict__ warp_len;
+};
+
+// outcome of one antidiagonal step
+enum : int { kGo = 0, kDone = 1, kBand = 2, kEscalate = 3 };
+
+}  // namespace xb

@@ -1,0 +1,70 @@
+"""The five BASELINE.json configs as deterministic synthetic inputs (C++ generator,
+csrc/xb_synth.cpp).  Returns the pool as (symbols uint8, offsets int64) plus
+tasks (n, 4) int64 = (h_id, v_id, h_seed, v_seed)."""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from .capi import check, lib
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+BLOSUM62_JSON = os.path.join(os.path.dirname(HERE), "tests", "golden", "blosum62.json")
+
+
+def blosum62_text() -> str:
+    """NCBI-format BLOSUM62 text rebuilt from the committed fixture."""
+    with open(BLOSUM62_JSON) as f:
+        m = json.load(f)
+    alpha, cells = m["alphabet"], m["cells"]
+    n = len(alpha)
+    lines = ["   " + "  ".join(alpha)]
+    for i, a in enumerate(alpha):
+        lines.append(a + " " + " ".join(f"{cells[i * n + j]:2d}" for j in range(n)))
+    return "\n".join(lines) + "\n"
+
+
+@dataclass
+class Dataset:
+    cfg: int
+    symbols: np.ndarray
+    offsets: np.ndarray
+    tasks: np.ndarray
+    k: int
+    x: int
+    band: int
+
+    @property
+    def n_tasks(self) -> int:
+        return len(self.tasks)
+
+    def seq(self, i: int) -> bytes:
+        return self.symbols[self.offsets[i]:self.offsets[i + 1]].tobytes()
+
+    def paper_products(self) -> float:
+        """sum over tasks of |H| * |V| (pipeline.cpp:156-162)."""
+        ln = np.diff(self.offsets).astype(np.float64)
+        return float(np.sum(ln[self.tasks[:, 0]] * ln[self.tasks[:, 1]]))
+
+
+def make(cfg: int, scale: float = 1.0, seed: int = 0, threads: int = 0) -> Dataset:
+    L = lib()
+    err = C.c_int(0)
+    mtext = blosum62_text().encode() if cfg == 3 else None
+    h = L.xb_synth_make(cfg, scale, seed, mtext, threads, C.byref(err))
+    check(err.value, "xb_synth_make")
+    try:
+        z = (C.c_int64 * 6)()
+        L.xb_synth_sizes(h, z)
+        n_seqs, total, n_tasks, k, x, band = (int(v) for v in z)
+        sym = np.empty(total, dtype=np.uint8)
+        off = np.empty(n_seqs + 1, dtype=np.int64)
+        tasks = np.empty((n_tasks, 4), dtype=np.int64)
+        L.xb_synth_copy(h, sym.ctypes.data, off.ctypes.data, tasks.ctypes.data)
+    finally:
+        L.xb_synth_free(h)
+    return Dataset(cfg, sym, off, tasks, k, x, band)

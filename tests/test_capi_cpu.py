@@ -1,0 +1,118 @@
+"""CPU: the C-ABI library loads, exports every declared symbol, validates
+inputs like the reference, packs pools, and generates the configs
+deterministically.  No kernel is launched here (no GPU in this container)."""
+import ctypes as C
+import hashlib
+import re
+
+import numpy as np
+import pytest
+
+from helpers import blosum62, load_json
+
+import paper_2304_08662_b200 as xb
+from paper_2304_08662_b200 import capi, synth
+
+
+def test_exports_match_header():
+    hdr = open(capi.os.path.join(capi.os.path.dirname(capi.HERE), "include", "xdrop_b200.h")).read()
+    declared = set(re.findall(r"\b(xb_[a-z0-9_]+)\s*\(", hdr))
+    assert declared == set(capi.EXPORTED)
+    L = capi.lib()
+    for name in declared:
+        assert hasattr(L, name), name
+    assert L.xb_version().decode().startswith("xdrop_b200")
+
+
+def test_parse_submatrix_matches_reference():
+    a, c = blosum62()  # produced by the reference's parse_submatrix
+    m = xb.parse_submatrix(synth.blosum62_text())
+    assert m.alphabet == a and m.cells == c
+    s = xb.ScoringScheme.from_matrix(m, -1, 20)
+    assert s.sim("A", "A") == 4 and s.sim("W", "W") == 11 and s.sim("*", "*") == 1  # test_scoring.cpp:89-98
+    assert all(s.sim(p, q) == s.sim(q, p) for p in a for q in a)
+    with pytest.raises(xb.UnknownSymbol):
+        s.sim("a", "A")
+    with pytest.raises(xb.InputError):
+        xb.parse_submatrix("   A  B\nA 1 2\nB 1\n")  # NonSquare
+    with pytest.raises(xb.InputError):
+        xb.parse_submatrix("   A  B\nB 1 2\nA 1 2\n")  # row order != header
+
+
+def test_scheme_validation_and_n_rule():
+    with pytest.raises(xb.InputError):
+        xb.ScoringScheme.match_mismatch(0, -1, -1, 3)
+    with pytest.raises(xb.InputError):
+        xb.ScoringScheme.match_mismatch(1, 1, -1, 3)
+    with pytest.raises(xb.InputError):
+        xb.ScoringScheme.match_mismatch(1, -1, 0, 3)
+    with pytest.raises(xb.InputError):
+        xb.ScoringScheme.match_mismatch(1, -1, -1, -1)
+    s = xb.ScoringScheme.match_mismatch(2, -3, -1, 3)
+    assert s.sim("A", "A") == 2 and s.sim("A", "C") == -3
+    assert s.sim("N", "N") == -3  # N never matches (scoring.cpp:25-31)
+
+
+def test_pool_packing_choice_and_validation():
+    s = xb.ScoringScheme.match_mismatch(1, -1, -1, 5)
+    p = xb.DevicePool(s, b"ACGTACGT", np.array([0, 4, 8]))
+    assert p.bits_per_symbol == 2
+    p2 = xb.DevicePool(s, b"ACGNACGT", np.array([0, 4, 8]))
+    assert p2.bits_per_symbol == 5
+    with pytest.raises(xb.UnknownSymbol):
+        xb.DevicePool(s, b"ACGUACGT", np.array([0, 4, 8]))
+    with pytest.raises(xb.UnknownSymbol):
+        xb.DevicePool(s, b"acgt", np.array([0, 4]))
+
+
+def test_task_validation_precedes_device():
+    s = xb.ScoringScheme.match_mismatch(1, -1, -1, 5)
+    p = xb.DevicePool(s, b"ACGTACGT", np.array([0, 4, 8]))
+    with pytest.raises(xb.DanglingReference):
+        xb.extend_tasks(p, np.array([[0, 7, 0, 0]]), 2, 8)
+    with pytest.raises(xb.SeedOutOfBounds):
+        xb.extend_tasks(p, np.array([[0, 1, 3, 0]]), 2, 8)
+    with pytest.raises(xb.SeedOutOfBounds):
+        xb.extend_tasks(p, np.array([[0, 1, 0, 4]]), 1, 8)
+    with pytest.raises(xb.InputError):
+        xb.extend_tasks(p, np.array([[0, 1, 0, 0]]), 1, 0)  # band < 1
+
+
+def test_no_cpu_fallback():
+    if capi.lib().xb_device_count() > 0:
+        pytest.skip("a GPU is visible")
+    s = xb.ScoringScheme.match_mismatch(1, -1, -1, 5)
+    p = xb.DevicePool(s, b"ACGTACGT", np.array([0, 4, 8]))
+    with pytest.raises(xb.xband.DeviceError, match="no CUDA device"):
+        xb.extend_tasks(p, np.array([[0, 1, 0, 0]]), 2, 8)
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_synth_matches_golden_inputs(cfg):
+    meta = load_json("configs_meta.json")[str(cfg)]
+    ds = synth.make(cfg, meta["scale"])
+    h = hashlib.sha256(ds.symbols.tobytes() + ds.offsets.tobytes() + ds.tasks.tobytes()).hexdigest()
+    assert h == meta["input_sha256"]
+    assert (ds.k, ds.x, ds.band) == (meta["k"], meta["x"], meta["band"])
+    # seeds are exact k-mers on both sides
+    for t in ds.tasks[:50]:
+        a = ds.symbols[ds.offsets[t[0]] + t[2]: ds.offsets[t[0]] + t[2] + ds.k]
+        b = ds.symbols[ds.offsets[t[1]] + t[3]: ds.offsets[t[1]] + t[3] + ds.k]
+        assert (a == b).all()
+
+
+def test_synth_thread_count_invariance():
+    a = synth.make(5, 0.0003, threads=1)
+    b = synth.make(5, 0.0003, threads=8)
+    assert (a.symbols == b.symbols).all() and (a.tasks == b.tasks).all()
+
+
+def test_split_lr_mirror():
+    # partition.cpp:45-81 / test_partition.cpp:69-105 shape
+    store = xb.SequenceStore([xb.Sequence(0, "h", "A" * 100), xb.Sequence(1, "v", "A" * 80)])
+    l, r = xb.split_lr(xb.ExtensionTask(3, 0, 1, 30, 20), store, 17)
+    assert (l.unit_id, l.h_len, l.v_len, l.est_cost) == (6, 30, 20, 600)
+    assert (r.unit_id, r.h_origin, r.v_origin, r.h_len, r.v_len) == (7, 47, 37, 53, 43)
+    with pytest.raises(xb.SeedOutOfBounds):
+        xb.split_lr(xb.ExtensionTask(0, 0, 1, 90, 0), store, 17)
+    assert xb.gcups(1000, 1000, 1e-3) == pytest.approx(1.0)

@@ -1,0 +1,242 @@
+"""GPU parity: the sm_100a engine, called through the C-ABI, against the
+reference's golden vectors and the C oracle.  Bar: bit-exact on every field
+(score, h_ext, v_ext, cells, delta_w; spread + cells on band failures)."""
+import hashlib
+import os
+import random
+
+import numpy as np
+import pytest
+
+from helpers import blosum62, expect_tuple, load_json, oracle_scheme, rec_tuple, result_rows_equal
+
+pytestmark = pytest.mark.gpu
+
+VEC = load_json("kernel_vectors.json")
+
+
+@pytest.fixture(scope="module")
+def xb():
+    import paper_2304_08662_b200 as xb
+    assert xb.capi.lib().xb_device_count() > 0, "no CUDA device: the engine has no CPU fallback"
+    return xb
+
+
+def _scheme(xb, spec):
+    if spec[0] == "BLOSUM62":
+        a, c = blosum62()
+        return xb.ScoringScheme.from_matrix(xb.SubMatrix(a, c), spec[1], spec[2])
+    return xb.ScoringScheme.match_mismatch(*spec)
+
+
+def _units_for(xb, entries):
+    """All entries of one scheme as explicit units over one pool."""
+    from paper_2304_08662_b200.capi import UNIT_DTYPE
+    syms, off = [], [0]
+    units = np.zeros(len(entries), dtype=UNIT_DTYPE)
+    for q, e in enumerate(entries):
+        h, v = e["h"].encode(), e["v"].encode()
+        syms += [h, v]
+        off += [off[-1] + len(h), off[-1] + len(h) + len(v)]
+        kw = e["kw"]
+        hd, vd = kw.get("h_dir", 1), kw.get("v_dir", 1)
+        ho, vo = kw.get("h_origin", 0), kw.get("v_origin", 0)
+        units[q] = (2 * q, 2 * q + 1, hd, vd, ho, vo,
+                    (len(h) - ho) if hd else ho, (len(v) - vo) if vd else vo)
+    return b"".join(syms), np.array(off, dtype=np.int64), units
+
+
+def _by_scheme(entries):
+    groups = {}
+    for i, e in enumerate(entries):
+        spec = tuple(e.get("scheme", [1, -1, -1, e["x"]]))
+        groups.setdefault((spec, e["band"]), []).append(i)
+    return groups
+
+
+@pytest.mark.parametrize("flags", [0, 2, 4], ids=["cascade", "warp_tier_only", "tier64_first"])
+def test_vectors_all_tiers(xb, flags):
+    entries = VEC["kats"] + VEC["random"]
+    bad = []
+    for (spec, band), idx in _by_scheme(entries).items():
+        sel = [entries[i] for i in idx]
+        sym, off, units = _units_for(xb, sel)
+        pool = xb.DevicePool(_scheme(xb, list(spec)), sym, off)
+        out = xb.extend_units(pool, units, band, exec_flags=flags)
+        for i, r in zip(idx, out):
+            if rec_tuple(r) != expect_tuple(entries[i]["kernel"]):
+                bad.append((i, rec_tuple(r), expect_tuple(entries[i]["kernel"])))
+    assert not bad, f"{len(bad)} mismatches: {bad[:4]}"
+
+
+def test_reference_api_kats(xb):
+    # proj/tests/test_align.cpp:41-123 in the reference's own vocabulary
+    S, full = xb.Sequence, xb.full
+    s3 = xb.ScoringScheme.match_mismatch(1, -1, -1, 3)
+    a = S(0, "s", "ACGT")
+    r = xb.xdrop_extend(full(a), full(a), s3, 16)
+    assert (r.score, r.h_ext, r.v_ext) == (4, 4, 4)
+    r = xb.xdrop_extend(full(S(0, "h", "")), full(S(1, "v", "ACGT")), s3, 8)
+    assert (r.score, r.h_ext, r.v_ext) == (0, 0, 0)
+    e = S(0, "e", "")
+    r = xb.xdrop_extend(full(e), full(e), s3, 4)
+    assert r.cells == 1 and r.delta_w == 1
+    s10 = xb.ScoringScheme.match_mismatch(1, -1, -1, 10)
+    r = xb.xdrop_extend(full(S(0, "h", "AAAAAA")), full(S(1, "v", "AATAAA")), s10, 16)
+    assert (r.score, r.h_ext, r.v_ext) == (4, 5, 6)
+    with pytest.raises(xb.BandExceededError) as ei:
+        xb.xdrop_extend(full(S(0, "h", "AAAAAA")), full(S(1, "v", "AATAAA")), s10, 2)
+    assert ei.value.observed_spread == 3 and ei.value.cells == 3
+    with pytest.raises(xb.InputError):
+        xb.xdrop_extend(full(a), full(a), s3, 16, scratch=xb.BandBuffers(8))
+    with pytest.raises(xb.InputError):
+        xb.BandBuffers(0)
+
+
+def test_seed_extension(xb):
+    # align.cpp:268-309; test_align.cpp:243-302
+    for e in VEC["seeds"]:
+        store = xb.SequenceStore([xb.Sequence(0, "h", e["h"]), xb.Sequence(1, "v", e["v"])])
+        t = xb.ExtensionTask(0, e["h_id"], e["v_id"], e["h_seed"], e["v_seed"])
+        s = xb.ScoringScheme.match_mismatch(1, -1, -1, e["x"])
+        if e["rc"] == 2:
+            with pytest.raises(xb.DanglingReference):
+                xb.extend_seed(t, store, e["k"], s, e["band"])
+        elif e["rc"] == 3:
+            with pytest.raises(xb.SeedOutOfBounds):
+                xb.extend_seed(t, store, e["k"], s, e["band"])
+        elif e["rc"] == 1:
+            with pytest.raises(xb.BandExceededError) as ei:
+                xb.extend_seed(t, store, e["k"], s, e["band"])
+            assert ei.value.side == e["side"] and ei.value.observed_spread == e["spread"]
+        else:
+            a = xb.extend_seed(t, store, e["k"], s, e["band"])
+            assert a.seed_score == e["seed_score"] and a.total == e["total"]
+            assert _er(a.left) == expect_tuple(e["left"])
+            assert _er(a.right) == expect_tuple(e["right"])
+
+
+def _er(r):
+    return (r.score, r.h_ext, r.v_ext, r.cells, r.delta_w)
+
+
+def _config_pool(xb, ds):
+    if ds.cfg == 3:
+        a, c = blosum62()
+        s = xb.ScoringScheme.from_matrix(xb.SubMatrix(a, c), -1, ds.x)
+    else:
+        s = xb.ScoringScheme.match_mismatch(1, -1, -1, ds.x)
+    return xb.DevicePool(s, ds.symbols, ds.offsets)
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("flags", [0, 1, 2], ids=["cascade", "unsorted", "warp_tier_only"])
+def test_configs_vs_reference_golden(xb, cfg, flags):
+    from paper_2304_08662_b200 import synth
+    meta = load_json("configs_meta.json")[str(cfg)]
+    ds = synth.make(cfg, meta["scale"])
+    h = hashlib.sha256(ds.symbols.tobytes() + ds.offsets.tobytes() + ds.tasks.tobytes()).hexdigest()
+    assert h == meta["input_sha256"]
+    ref = np.load(os.path.join(os.path.dirname(__file__), "golden", f"cfg{cfg}_ref.npz"))
+    pool = _config_pool(xb, ds)
+    out, ss = xb.extend_tasks(pool, ds.tasks, ds.k, ds.band, exec_flags=flags)
+    eq = result_rows_equal(out, ref["results"])
+    assert eq.all(), f"{(~eq).sum()} of {len(eq)} sides differ; first {np.nonzero(~eq)[0][:5]}"
+    assert (ss == ref["seed_score"]).all()
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_configs_sample_vs_oracle_full_size(xb, oracle, cfg):
+    """BASELINE-size inputs: a seeded sample of tasks checked against the
+    oracle, and the whole batch checked for run-to-run identity."""
+    from paper_2304_08662_b200 import synth
+    scale = {1: 1.0, 2: 0.2, 3: 1.0, 4: 0.1, 5: 0.02}[cfg]
+    ds = synth.make(cfg, scale)
+    pool = _config_pool(xb, ds)
+    rng = np.random.default_rng(cfg)
+    pick = np.sort(rng.choice(ds.n_tasks, size=min(ds.n_tasks, 300), replace=False))
+    out, ss = xb.extend_tasks(pool, ds.tasks[pick], ds.k, ds.band)
+    s = oracle_scheme(oracle, ["BLOSUM62", -1, ds.x] if cfg == 3 else [1, -1, -1, ds.x])
+    exp, ess = oracle.extend_batch(ds.symbols, ds.offsets, ds.tasks[pick], ds.k, s, ds.band,
+                                   threads=os.cpu_count() or 1)
+    assert result_rows_equal(out, exp).all()
+    assert (ss == ess).all()
+    a, _ = xb.extend_tasks(pool, ds.tasks, ds.k, ds.band)
+    b, _ = xb.extend_tasks(pool, ds.tasks, ds.k, ds.band, exec_flags=1)
+    assert result_rows_equal(a, b).all()
+    # every sampled row inside the full run equals the sampled run
+    full = a.reshape(-1, 2)[pick].reshape(-1)
+    assert result_rows_equal(full, out).all()
+
+
+def test_swap_symmetry_full_size(xb):
+    """Size-independent property: swapping h and v (symmetric scoring) keeps
+    score, cells and delta_w (the window rules are symmetric in i and j)."""
+    from paper_2304_08662_b200 import synth
+    ds = synth.make(2, 0.05)
+    pool = _config_pool(xb, ds)
+    sw = ds.tasks[:, [1, 0, 3, 2]]
+    a, sa = xb.extend_tasks(pool, ds.tasks, ds.k, ds.band)
+    b, sb = xb.extend_tasks(pool, sw, ds.k, ds.band)
+    for f in ("score", "cells", "delta_w", "status"):
+        assert (a[f] == b[f]).all(), f
+    assert (sa == sb).all()
+
+
+def test_band_failures_and_escalation(xb, oracle):
+    """Wide windows: X large so spreads exceed 32 and 64 slots (tier escalation)
+    and a band small enough that some sides fail with exact spread/cells."""
+    rng = random.Random(7)
+    entries = []
+    for it in range(120):
+        n = rng.randint(50, 900)
+        h = bytes(rng.choice(b"ACGT") for _ in range(n))
+        v = bytearray(h)
+        for q in range(len(v)):
+            if rng.random() < 0.25:
+                v[q] = rng.choice(b"ACGT")
+        entries.append((h, bytes(v)))
+    for x, band in ((60, 1000), (120, 1000), (60, 70), (30, 40)):
+        so = oracle.scheme_mm(1, -1, -1, x)
+        sym = b"".join(h + v for h, v in entries)
+        off = [0]
+        for h, v in entries:
+            off += [off[-1] + len(h), off[-1] + len(h) + len(v)]
+        from paper_2304_08662_b200.capi import UNIT_DTYPE
+        units = np.zeros(len(entries), dtype=UNIT_DTYPE)
+        for q, (h, v) in enumerate(entries):
+            units[q] = (2 * q, 2 * q + 1, 1, 1, 0, 0, len(h), len(v))
+        pool = xb.DevicePool(xb.ScoringScheme.match_mismatch(1, -1, -1, x), sym, np.array(off))
+        out = xb.extend_units(pool, units, band)
+        for q, (h, v) in enumerate(entries):
+            assert rec_tuple(out[q]) == rec_tuple(oracle.extend(h, v, so, band)), (x, band, q)
+
+
+def test_pipeline_drop_in(xb):
+    """The reference pipeline's result rows (pipeline.cpp:99-137 +
+    io.cpp:258-298) rebuilt from the batch API on the reference's own synthetic
+    dataset equal the reference's rows byte for byte."""
+    import ctypes  # noqa: F401
+    rows = load_json("pipeline_rows.json")
+    from oracle_py import REF_SO, Ref
+    for name, p in rows.items():
+        if not os.path.exists(REF_SO):
+            pytest.skip("reference dataset generator not available on this host")
+        R = Ref()
+        sym, off, tasks = R.generate_synthetic(p["pairs"], p["length"], p["p_match"], p["k"],
+                                               p["seed"], p.get("uniform_seed", False))
+        store = xb.SequenceStore(
+            [xb.Sequence(i, "s", sym[off[i]:off[i + 1]].tobytes().decode()) for i in range(len(off) - 1)])
+        tl = [xb.ExtensionTask(t, *map(int, tasks[t])) for t in range(len(tasks))]
+        s = xb.ScoringScheme.match_mismatch(1, -1, -1, p["x"])
+        al, failed, _ = xb.extend_batch(store, tl, p["k"], s, p["band"])
+        got = ["task_id\tside\tscore\th_ext\tv_ext\tcells\tdelta_w"]
+        tot = 0
+        for a in al:
+            for side, r in (("L", a.left), ("R", a.right)):
+                got.append(f"{a.task_id}\t{side}\t{r.score}\t{r.h_ext}\t{r.v_ext}\t{r.cells}\t{r.delta_w}")
+            tot += a.total
+        got.append(f"# total\t{tot}")
+        for f in failed:
+            got.append(f"# failed\ttask {f.task_id} side {f.side} spread {f.observed_spread}")
+        assert got == p["rows"], name
