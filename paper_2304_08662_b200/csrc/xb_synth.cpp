@@ -279,7 +279,7 @@ int make_protein(xb_synth* S, double scale, uint64_t seed, const char* matrix_te
 void make_overlap(xb_synth* S, double scale, uint64_t seed, int T) {
     const int64_t n_reads = std::max<int64_t>(4, llround(200000 * scale));
     const int64_t want = std::max<int64_t>(1, llround(2000000 * scale));
-    const int64_t G = n_reads * 1100;
+    const int64_t G = n_reads * 900;
     const int k = 17;
     Rng master(splitmix(seed));
     std::vector<int64_t> len(static_cast<size_t>(n_reads)), start(static_cast<size_t>(n_reads));

@@ -169,18 +169,38 @@ def test_configs_sample_vs_oracle_full_size(xb, oracle, cfg):
     assert result_rows_equal(full, out).all()
 
 
-def test_swap_symmetry_full_size(xb):
-    """Size-independent property: swapping h and v (symmetric scoring) keeps
-    score, cells and delta_w (the window rules are symmetric in i and j)."""
+def test_x_monotone_full_size(xb):
+    """Size-independent property at BASELINE lengths (acceptance.cpp:355-375,
+    test_align.cpp:186-200): raising X never lowers the score nor narrows the
+    spread while the band suffices."""
     from paper_2304_08662_b200 import synth
     ds = synth.make(2, 0.05)
-    pool = _config_pool(xb, ds)
-    sw = ds.tasks[:, [1, 0, 3, 2]]
-    a, sa = xb.extend_tasks(pool, ds.tasks, ds.k, ds.band)
-    b, sb = xb.extend_tasks(pool, sw, ds.k, ds.band)
-    for f in ("score", "cells", "delta_w", "status"):
-        assert (a[f] == b[f]).all(), f
-    assert (sa == sb).all()
+    res = []
+    for x in (5, 15, 40):
+        pool = xb.DevicePool(xb.ScoringScheme.match_mismatch(1, -1, -1, x), ds.symbols, ds.offsets)
+        res.append(xb.extend_tasks(pool, ds.tasks, ds.k, 1024)[0])
+    for lo, hi in zip(res, res[1:]):
+        ok = (lo["status"] == 0) & (hi["status"] == 0)
+        assert ok.mean() > 0.99
+        assert (hi["score"][ok] >= lo["score"][ok]).all()
+        assert (hi["delta_w"][ok] >= lo["delta_w"][ok]).all()
+
+
+def test_self_extension_full_length(xb):
+    """Perfect matches extend to the full view whatever the length
+    (test_align.cpp:202-213): score = length, spread independent of length."""
+    from paper_2304_08662_b200 import synth
+    ds = synth.make(5, 0.0005)
+    n = len(ds.offsets) - 1
+    pool = xb.DevicePool(xb.ScoringScheme.match_mismatch(1, -1, -1, 6), ds.symbols, ds.offsets)
+    t = np.zeros((n, 4), dtype=np.int64)
+    t[:, 0] = t[:, 1] = np.arange(n)
+    out, ss = xb.extend_tasks(pool, t, 0, 64)
+    ln = np.diff(ds.offsets)
+    right = out[1::2]
+    assert (right["status"] == 0).all()
+    assert (right["score"] == ln).all() and (right["h_ext"] == ln).all() and (right["v_ext"] == ln).all()
+    assert len(set(right["delta_w"].tolist())) == 1
 
 
 def test_band_failures_and_escalation(xb, oracle):
