@@ -163,13 +163,13 @@ def main():
     # ---- the reference pipeline on its own synthetic data (Appendix B) ----
     ec, txt = R.pipeline_synth(8, 2000, 0.9, x=15)
     rows = [l for l in txt.splitlines() if not l.startswith("#") or l.startswith("# total\t")
-            or l.startswith("# failed")]
+            or l.startswith("# failed\t")]
     pipe = {"pairs": 8, "length": 2000, "p_match": 0.9, "x": 15, "band": 1024, "k": 17,
             "seed": 42, "exit_code": ec, "sha256_full": hashlib.sha256(txt.encode()).hexdigest(),
             "rows": rows}
     ec2, txt2 = R.pipeline_synth(40, 3000, 0.75, x=25, band=40, seed=7, uniform_seed=True)
     rows2 = [l for l in txt2.splitlines() if not l.startswith("#") or l.startswith("# total\t")
-             or l.startswith("# failed")]
+             or l.startswith("# failed\t")]
     pipe2 = {"pairs": 40, "length": 3000, "p_match": 0.75, "x": 25, "band": 40, "k": 17,
              "seed": 7, "uniform_seed": True, "exit_code": ec2, "rows": rows2}
     json.dump({"readme_smoke": pipe, "band_failures": pipe2},
