@@ -79,21 +79,24 @@ typedef struct {
 
 #define XB_FLAG_NO_SORT 1       /* skip the longest-first cost sort (ablation) */
 #define XB_FLAG_GENERIC_ONLY 2  /* route every unit to the warp tier (testing) */
-#define XB_FLAG_TIER2_FIRST 4   /* start at the 64-slot thread tier (testing) */
+#define XB_FLAG_FORCE_TIER 8    /* start at thread tier (flags >> 8) & 15, no pilot (testing) */
 
-/* Per-call device statistics (host-side view, summed over devices). */
+/* Per-call device statistics (summed over devices; times are the max).
+ * Tiers: 0..4 = one unit per thread with a K = 16/24/32/48/64 slot band,
+ * 5 = one warp per unit (exact generic path). */
 typedef struct {
     int32_t n_devices;
     int32_t launches;            /* kernels launched by the last run */
-    double ms_total;             /* device time of the whole run (max over devices) */
-    double ms_prep;              /* LR split + seed scores + sort */
-    double ms_tier[3];           /* thread tier K=32, thread tier K=64, warp tier */
-    int64_t units_tier[3];       /* units finished per tier */
-    int64_t cells_tier[3];       /* sum of ExtensionResult.cells finished per tier */
-    int64_t escalated[2];        /* units pushed out of tier 0 / tier 1 */
+    double ms_total;             /* device time of the whole run */
+    double ms_prep;              /* LR split + seed scores + cost sort */
+    double ms_pilot;             /* pilot sample + start-tier choice */
+    double ms_tier[6];
+    int64_t units_tier[6];       /* units finished per tier */
+    int64_t cells_tier[6];       /* sum of ExtensionResult.cells finished per tier */
+    int64_t escalated[6];        /* units handed from tier t to tier t+1 */
     int64_t h2d_bytes, d2h_bytes;
     int32_t sm_count;
-    int32_t pad;
+    int32_t start_tier;          /* tier the pilot chose */
 } xb_stats;
 
 typedef struct xb_scheme xb_scheme;

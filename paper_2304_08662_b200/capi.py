@@ -30,7 +30,11 @@ XB_SIDE_BAND_EXCEEDED = 1
 
 XB_FLAG_NO_SORT = 1
 XB_FLAG_GENERIC_ONLY = 2
-XB_FLAG_TIER2_FIRST = 4
+XB_FLAG_FORCE_TIER = 8
+
+
+def force_tier(t: int) -> int:
+    return XB_FLAG_FORCE_TIER | (t << 8)
 
 # numpy views of the C structs
 TASK_DTYPE = np.dtype([("task_id", "<i4"), ("h_id", "<u4"), ("v_id", "<u4"), ("pad", "<u4"),
@@ -49,20 +53,23 @@ class XbExec(C.Structure):
                 ("stream", C.c_void_p), ("flags", C.c_int32)]
 
 
+TIER_NAMES = ["thread_k16", "thread_k24", "thread_k32", "thread_k48", "thread_k64", "warp"]
+
+
 class XbStats(C.Structure):
     _fields_ = [("n_devices", C.c_int32), ("launches", C.c_int32), ("ms_total", C.c_double),
-                ("ms_prep", C.c_double), ("ms_tier", C.c_double * 3),
-                ("units_tier", C.c_int64 * 3), ("cells_tier", C.c_int64 * 3),
-                ("escalated", C.c_int64 * 2), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
-                ("sm_count", C.c_int32), ("pad", C.c_int32)]
+                ("ms_prep", C.c_double), ("ms_pilot", C.c_double), ("ms_tier", C.c_double * 6),
+                ("units_tier", C.c_int64 * 6), ("cells_tier", C.c_int64 * 6),
+                ("escalated", C.c_int64 * 6), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
+                ("sm_count", C.c_int32), ("start_tier", C.c_int32)]
 
     def as_dict(self) -> dict:
         return {"n_devices": self.n_devices, "launches": self.launches,
-                "ms_total": self.ms_total, "ms_prep": self.ms_prep,
+                "ms_total": self.ms_total, "ms_prep": self.ms_prep, "ms_pilot": self.ms_pilot,
                 "ms_tier": list(self.ms_tier), "units_tier": list(self.units_tier),
                 "cells_tier": list(self.cells_tier), "escalated": list(self.escalated),
                 "h2d_bytes": self.h2d_bytes, "d2h_bytes": self.d2h_bytes,
-                "sm_count": self.sm_count}
+                "sm_count": self.sm_count, "start_tier": self.start_tier}
 
 
 _lib = None

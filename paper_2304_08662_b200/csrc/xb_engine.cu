@@ -29,6 +29,7 @@ template <int K, int MODE>
 __global__ void thread_tier_kernel(TierParams P);
 template <int ENC>
 __global__ void warp_tier_kernel(TierParams P);
+__global__ void select_tier_kernel(TierParams P, int forced);
 __global__ void prep_kernel(PrepParams P);
 __global__ void int_peak_alu(int32_t* out, int iters, int32_t seed, long long* clk);
 __global__ void int_peak_mixed(int32_t* out, int iters, int32_t seed, long long* clk);
@@ -472,15 +473,16 @@ struct DevBatch {
     uint32_t *d_keys = nullptr, *d_vals = nullptr, *d_keys2 = nullptr, *d_order = nullptr;
     DevResult* d_res = nullptr;
     int32_t* d_seed = nullptr;
-    uint32_t *d_list1 = nullptr, *d_list2 = nullptr;
+    uint32_t* d_lists = nullptr;  // kNumTiers x n_units escalation inputs
     DevCounters* d_ctr = nullptr;
     int32_t* d_scratch = nullptr;
     int scratch_warps = 0;
     void* d_cub = nullptr;
     size_t cub_bytes = 0;
-    cudaEvent_t ev[6] = {};
+    cudaEvent_t ev[12] = {};
     int sm_count = 0;
-    int occ[2] = {0, 0};
+    int occ[5] = {0, 0, 0, 0, 0};
+    int mode = 0;
     int launches = 0;
     // host staging (pinned)
     DevResult* h_res = nullptr;
@@ -509,8 +511,7 @@ static void free_dev(DevBatch& D) {
     cudaFree(D.d_order);
     cudaFree(D.d_res);
     cudaFree(D.d_seed);
-    cudaFree(D.d_list1);
-    cudaFree(D.d_list2);
+    cudaFree(D.d_lists);
     cudaFree(D.d_ctr);
     cudaFree(D.d_scratch);
     cudaFree(D.d_cub);
@@ -548,8 +549,7 @@ static int setup_device(xb_batch* B, DevBatch& D, const xb_exec* ex) {
     CK(cudaMalloc(&D.d_keys2, U * 4));
     CK(cudaMalloc(&D.d_order, U * 4));
     CK(cudaMalloc(&D.d_res, U * sizeof(DevResult)));
-    CK(cudaMalloc(&D.d_list1, U * 4));
-    CK(cudaMalloc(&D.d_list2, U * 4));
+    CK(cudaMalloc(&D.d_lists, U * 4 * kNumTiers));
     CK(cudaMalloc(&D.d_ctr, sizeof(DevCounters)));
     CK(cudaMallocHost(&D.h_res, U * sizeof(DevResult)));
     if (!B->units_mode) {
@@ -603,23 +603,37 @@ static int upload_inputs(xb_batch* B, DevBatch& D, const void* items) {
 }
 
 template <int MODE>
-static void launch_thread_tier(int K, const TierParams& P, int blocks, cudaStream_t st) {
-    if (K == 32)
-        thread_tier_kernel<32, MODE><<<blocks, kTB, 0, st>>>(P);
-    else
-        thread_tier_kernel<64, MODE><<<blocks, kTB, 0, st>>>(P);
+static cudaError_t launch_thread_tier(int t, const TierParams& P, int blocks, cudaStream_t st) {
+    switch (t) {
+        case 0: thread_tier_kernel<16, MODE><<<blocks, kTB, 0, st>>>(P); break;
+        case 1: thread_tier_kernel<24, MODE><<<blocks, kTB, 0, st>>>(P); break;
+        case 2: thread_tier_kernel<32, MODE><<<blocks, kTB, 0, st>>>(P); break;
+        case 3: thread_tier_kernel<48, MODE><<<blocks, kTB, 0, st>>>(P); break;
+        default: thread_tier_kernel<64, MODE><<<blocks, kTB, 0, st>>>(P); break;
+    }
+    return cudaGetLastError();
 }
 
-static int occupancy_blocks(int K, int mode, int* out) {
-    int b = 0;
-    cudaError_t e = cudaSuccess;
-#define OCC(KK, MM) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, thread_tier_kernel<KK, MM>, kTB, 0)
-    if (K == 32) {
-        if (mode == 0) OCC(32, 0); else if (mode == 1) OCC(32, 1); else OCC(32, 2);
-    } else {
-        if (mode == 0) OCC(64, 0); else if (mode == 1) OCC(64, 1); else OCC(64, 2);
+static cudaError_t launch_tier(int mode, int t, const TierParams& P, int blocks, cudaStream_t st) {
+    if (mode == 0) return launch_thread_tier<0>(t, P, blocks, st);
+    if (mode == 1) return launch_thread_tier<1>(t, P, blocks, st);
+    return launch_thread_tier<2>(t, P, blocks, st);
+}
+
+template <int MODE>
+static cudaError_t occ_mode(int t, int* b) {
+    switch (t) {
+        case 0: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(b, thread_tier_kernel<16, MODE>, kTB, 0);
+        case 1: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(b, thread_tier_kernel<24, MODE>, kTB, 0);
+        case 2: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(b, thread_tier_kernel<32, MODE>, kTB, 0);
+        case 3: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(b, thread_tier_kernel<48, MODE>, kTB, 0);
+        default: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(b, thread_tier_kernel<64, MODE>, kTB, 0);
     }
-#undef OCC
+}
+
+static int occupancy_blocks(int t, int mode, int* out) {
+    int b = 0;
+    const cudaError_t e = mode == 0 ? occ_mode<0>(t, &b) : mode == 1 ? occ_mode<1>(t, &b) : occ_mode<2>(t, &b);
     if (e != cudaSuccess) return XB_E_CUDA;
     *out = std::max(1, b);
     return XB_OK;
@@ -635,7 +649,7 @@ static int run_device(xb_batch* B, DevBatch& D) {
     CK(cudaMemsetAsync(D.d_ctr, 0, sizeof(DevCounters), D.stream));
     const int64_t nu = D.n_units;
     if (nu == 0) {
-        for (int q = 1; q < 6; ++q) CK(cudaEventRecord(D.ev[q], D.stream));
+        for (int q = 1; q < 9; ++q) CK(cudaEventRecord(D.ev[q], D.stream));
         return XB_OK;
     }
     // ---- LR split + seed score + cost keys (or host-built units) ----
@@ -657,8 +671,8 @@ static int run_device(xb_batch* B, DevBatch& D) {
         pp.keys = D.d_keys;
         pp.vals = D.d_vals;
         pp.seed_score = D.d_seed;
-        pp.warp_list = D.d_list2;
-        pp.warp_len = &D.d_ctr->list_len[2];
+        pp.warp_list = D.d_lists + int64_t(kWarpTier) * nu;
+        pp.warp_len = &D.d_ctr->list_len[kWarpTier];
         const int tb = 256;
         prep_kernel<<<unsigned((D.n_items + tb - 1) / tb), tb, 0, D.stream>>>(pp);
         CK(cudaGetLastError());
@@ -679,8 +693,9 @@ static int run_device(xb_batch* B, DevBatch& D) {
         CK(cudaMemcpyAsync(D.d_vals, vals.data(), size_t(nu) * 4, cudaMemcpyHostToDevice, D.stream));
         unsigned long long wlen = wl.size();
         if (!wl.empty())
-            CK(cudaMemcpyAsync(D.d_list2, wl.data(), wl.size() * 4, cudaMemcpyHostToDevice, D.stream));
-        CK(cudaMemcpyAsync(&D.d_ctr->list_len[2], &wlen, 8, cudaMemcpyHostToDevice, D.stream));
+            CK(cudaMemcpyAsync(D.d_lists + int64_t(kWarpTier) * nu, wl.data(), wl.size() * 4,
+                               cudaMemcpyHostToDevice, D.stream));
+        CK(cudaMemcpyAsync(&D.d_ctr->list_len[kWarpTier], &wlen, 8, cudaMemcpyHostToDevice, D.stream));
         CK(cudaStreamSynchronize(D.stream));  // host vectors die at scope end
     }
     // ---- longest first ----
@@ -697,62 +712,50 @@ static int run_device(xb_batch* B, DevBatch& D) {
     tp.pool = D.pool->words;
     tp.units = D.d_units;
     tp.results = D.d_res;
+    tp.order = order;
+    tp.lists = D.d_lists;
     tp.ctr = D.d_ctr;
     tp.scheme = D.pool->scheme;
+    tp.n_units = nu;
     tp.band = B->band;
-    tp.pat = 0x55555555u;
     tp.warp_scratch = D.d_scratch;
-    const bool skip_t0 = (B->flags & XB_FLAG_TIER2_FIRST) != 0;
-    // ---- tier 0: one thread per unit, 32-slot register band ----
-    if (!skip_t0 && !(B->flags & XB_FLAG_GENERIC_ONLY)) {
-        if (!D.occ[0]) CK(occupancy_blocks(32, mode, &D.occ[0]) ? cudaErrorUnknown : cudaSuccess);
-        tp.queue = order;
-        tp.queue_len_ptr = nullptr;
-        tp.queue_len = (unsigned long long)nu;
-        tp.esc_list = D.d_list1;
-        tp.esc_len = &D.d_ctr->list_len[1];
-        tp.tier = 0;
-        const int blocks = D.sm_count * D.occ[0];
-        if (mode == 0) launch_thread_tier<0>(32, tp, blocks, D.stream);
-        else if (mode == 1) launch_thread_tier<1>(32, tp, blocks, D.stream);
-        else launch_thread_tier<2>(32, tp, blocks, D.stream);
-        CK(cudaGetLastError());
+    tp.pat = 0x55555555u;
+    tp.r64 = 64;
+    tp.one = 1;
+    tp.zero = 0;
+    for (int f = 0; f < 16; ++f) tp.mulc[f] = f ? (1u << (32 - 2 * f)) : 0u;
+    // pilot sample: the middle of the longest-first order (unbiased widths,
+    // short enough not to stall the machine)
+    const int forced = (B->flags & XB_FLAG_FORCE_TIER) ? ((B->flags >> 8) & 15) : -1;
+    long long pn = (forced >= 0 || (B->flags & XB_FLAG_GENERIC_ONLY)) ? 0 : std::min<long long>(nu, 64 + nu / 256);
+    tp.pilot_lo = (nu - pn) / 2;
+    tp.pilot_hi = tp.pilot_lo + pn;
+    D.mode = mode;
+    for (int t = 0; t < 5; ++t)
+        if (!D.occ[t]) CK(occupancy_blocks(t, mode, &D.occ[t]) ? cudaErrorUnknown : cudaSuccess);
+    // ---- pilot on the widest thread tier, then pick the start tier ----
+    if (pn > 0) {
+        tp.tier = 4;
+        tp.pilot = 1;
+        const int blocks = int(std::min<long long>(D.sm_count * D.occ[4], (pn + kTB - 1) / kTB));
+        CK(launch_tier(mode, 4, tp, blocks, D.stream));
         ++D.launches;
     }
+    tp.pilot = 0;
+    select_tier_kernel<<<1, 32, 0, D.stream>>>(tp, forced >= 0 ? forced : (pn > 0 ? -1 : 4));
+    CK(cudaGetLastError());
+    ++D.launches;
     CK(cudaEventRecord(D.ev[2], D.stream));
-    // ---- tier 1: 64-slot register band for the units tier 0 could not hold ----
-    if (!(B->flags & XB_FLAG_GENERIC_ONLY)) {
-        if (!D.occ[1]) CK(occupancy_blocks(64, mode, &D.occ[1]) ? cudaErrorUnknown : cudaSuccess);
-        if (skip_t0) {
-            tp.queue = order;
-            tp.queue_len_ptr = nullptr;
-            tp.queue_len = (unsigned long long)nu;
-            tp.tier = 0;  // skip routed units like tier 0 does
-        } else {
-            tp.queue = D.d_list1;
-            tp.queue_len_ptr = &D.d_ctr->list_len[1];
-            tp.tier = 1;
-        }
-        tp.esc_list = D.d_list2;
-        tp.esc_len = &D.d_ctr->list_len[2];
-        const int blocks = D.sm_count * D.occ[1];
-        if (skip_t0) {
-            // count it under tier 1 in the stats: cursor slot 0 is still fresh
-        }
-        if (mode == 0) launch_thread_tier<0>(64, tp, blocks, D.stream);
-        else if (mode == 1) launch_thread_tier<1>(64, tp, blocks, D.stream);
-        else launch_thread_tier<2>(64, tp, blocks, D.stream);
-        CK(cudaGetLastError());
+    // ---- cascade: the start tier takes the queue, wider tiers their escalations ----
+    for (int t = 0; t < 5; ++t) {
+        tp.tier = t;
+        CK(launch_tier(mode, t, tp, D.sm_count * D.occ[t], D.stream));
         ++D.launches;
+        CK(cudaEventRecord(D.ev[3 + t], D.stream));
     }
-    CK(cudaEventRecord(D.ev[3], D.stream));
-    // ---- tier 2: warp per unit, exact generic path ----
+    // ---- warp per unit: exact generic path for whatever is left ----
     {
-        tp.queue = D.d_list2;
-        tp.queue_len_ptr = &D.d_ctr->list_len[2];
-        tp.tier = 2;
-        tp.esc_list = nullptr;
-        tp.esc_len = nullptr;
+        tp.tier = kWarpTier;
         const int blocks = D.scratch_warps / 4;
         if (p->enc == ENC_2BIT)
             warp_tier_kernel<ENC_2BIT><<<blocks, 128, 0, D.stream>>>(tp);
@@ -761,7 +764,7 @@ static int run_device(xb_batch* B, DevBatch& D) {
         CK(cudaGetLastError());
         ++D.launches;
     }
-    CK(cudaEventRecord(D.ev[4], D.stream));
+    CK(cudaEventRecord(D.ev[8], D.stream));
     return XB_OK;
 }
 
@@ -773,7 +776,7 @@ static int fetch_device(xb_batch* B, DevBatch& D) {
     if (!B->units_mode && D.n_items)
         CK(cudaMemcpyAsync(D.h_seed, D.d_seed, size_t(D.n_items) * 4, cudaMemcpyDeviceToHost,
                            D.stream));
-    CK(cudaEventRecord(D.ev[5], D.stream));
+    CK(cudaEventRecord(D.ev[9], D.stream));
     B->d2h += D.n_units * int64_t(sizeof(DevResult)) + (B->units_mode ? 0 : D.n_items * 4);
     return XB_OK;
 }
@@ -935,28 +938,30 @@ int xb_batch_stats(xb_batch* B, xb_stats* st) {
     if (!B || !st) return XB_E_BAD_PARAM;
     std::memset(st, 0, sizeof *st);
     st->n_devices = int(B->devs.size());
+    st->start_tier = -1;
     for (auto& D : B->devs) {
         CK(cudaSetDevice(D.dev));
         CK(cudaStreamSynchronize(D.stream));
         DevCounters c{};
         CK(cudaMemcpy(&c, D.d_ctr, sizeof c, cudaMemcpyDeviceToHost));
-        float ms[5] = {0, 0, 0, 0, 0};
+        float ms[10] = {0};
         if (D.n_units) {
-            CK(cudaEventElapsedTime(&ms[0], D.ev[0], D.ev[4]));
-            CK(cudaEventElapsedTime(&ms[1], D.ev[0], D.ev[1]));
-            CK(cudaEventElapsedTime(&ms[2], D.ev[1], D.ev[2]));
-            CK(cudaEventElapsedTime(&ms[3], D.ev[2], D.ev[3]));
-            CK(cudaEventElapsedTime(&ms[4], D.ev[3], D.ev[4]));
+            CK(cudaEventElapsedTime(&ms[0], D.ev[0], D.ev[8]));  // whole run
+            CK(cudaEventElapsedTime(&ms[1], D.ev[0], D.ev[1]));  // prep + sort
+            CK(cudaEventElapsedTime(&ms[2], D.ev[1], D.ev[2]));  // pilot + select
+            for (int t = 0; t < 5; ++t) CK(cudaEventElapsedTime(&ms[3 + t], D.ev[2 + t], D.ev[3 + t]));
+            CK(cudaEventElapsedTime(&ms[8], D.ev[7], D.ev[8]));  // warp tier
         }
         st->ms_total = std::max(st->ms_total, double(ms[0]));
         st->ms_prep = std::max(st->ms_prep, double(ms[1]));
-        for (int t = 0; t < 3; ++t) {
-            st->ms_tier[t] = std::max(st->ms_tier[t], double(ms[2 + t]));
+        st->ms_pilot = std::max(st->ms_pilot, double(ms[2]));
+        for (int t = 0; t < 6; ++t) {
+            st->ms_tier[t] = std::max(st->ms_tier[t], double(ms[3 + t]));
             st->units_tier[t] += int64_t(c.units[t]);
             st->cells_tier[t] += int64_t(c.cells[t]);
+            st->escalated[t] += int64_t(c.escalated[t]);
         }
-        st->escalated[0] += int64_t(c.escalated[0]);
-        st->escalated[1] += int64_t(c.escalated[1]);
+        st->start_tier = c.start_tier;
         st->launches += D.launches;
         st->sm_count = D.sm_count;
     }

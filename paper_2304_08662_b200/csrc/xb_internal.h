@@ -47,16 +47,19 @@ struct DevScheme {
     int32_t sim[32 * 32]; // code-pair scores [h][v] (sentinel row/col = very negative)
 };
 
-// Per-tier counters, device side.
+// Per-tier counters, device side (tiers: K16 K24 K32 K48 K64 warp).
 struct DevCounters {
-    unsigned long long cursor[3];     // work-queue cursors per tier
-    unsigned long long list_len[3];   // length of the escalation lists (tier 1, 2 inputs)
-    unsigned long long units[3];
-    unsigned long long cells[3];
-    unsigned long long escalated[2];
+    unsigned long long cursor[8];      // work-queue cursors per tier (slot 7: pilot)
+    unsigned long long list_len[8];    // escalation-input list lengths per tier
+    unsigned long long units[8];
+    unsigned long long cells[8];
+    unsigned long long escalated[8];
+    int32_t start_tier;                // chosen by the pilot
+    int32_t pad;
 };
 
 constexpr int kStatusOk = 0;
 constexpr int kStatusBand = 1;
+constexpr int kStatusEscalated = 2;  // transient: re-run by a wider tier
 
 }  // namespace xb

@@ -36,21 +36,34 @@ namespace xb {
 constexpr int32_t kDeadS = -(1 << 24);  // dead sentinel in drift space
 constexpr int kTB = 128;                // threads per block, thread tiers
 
+// Thread tiers: band widths K (slots per unit); index 5 is the warp tier.
+constexpr int kNumTiers = 6;
+constexpr int kWarpTier = 5;
+__host__ __device__ constexpr int tier_width(int t) {
+    return t == 0 ? 16 : t == 1 ? 24 : t == 2 ? 32 : t == 3 ? 48 : t == 4 ? 64 : 1 << 30;
+}
+
 struct TierParams {
     const uint32_t* __restrict__ pool;
     const DevUnit* __restrict__ units;
     DevResult* __restrict__ results;
-    const uint32_t* __restrict__ queue;  // unit indices to process
-    const unsigned long long* __restrict__ queue_len_ptr;  // device count (lists) or null
-    unsigned long long queue_len;        // static count when queue_len_ptr == null
-    uint32_t* __restrict__ esc_list;     // units that outgrow this tier
-    unsigned long long* __restrict__ esc_len;
+    const uint32_t* __restrict__ order;  // cost-sorted unit indices (main queue)
+    uint32_t* __restrict__ lists;        // kNumTiers segments of n_units: escalation inputs
     DevCounters* __restrict__ ctr;
     const DevScheme* __restrict__ scheme;
+    long long n_units;
+    long long pilot_lo, pilot_hi;        // order[pilot_lo, pilot_hi) is the pilot sample
     int32_t band;
-    int32_t tier;
+    int32_t tier;                        // this launch's tier index
+    int32_t pilot;                       // 1: run the pilot sample, 0: cascade
     int32_t* __restrict__ warp_scratch;  // warp tier: 2*band ints per warp slot
-    uint32_t pat;                        // 0x55555555, kept opaque so LOP3 takes it from c[]
+    // opaque constants: kept in c[]/uniform registers so ptxas cannot fold
+    // them into ALU-pipe forms (LEA, LOP3 immediates, SEL)
+    uint32_t pat;                        // 0x55555555
+    int32_t r64;                         // 64
+    int32_t one;                         // 1
+    int32_t zero;                        // 0
+    uint32_t mulc[16];                   // 2^(32-2f), f = 1..15
 };
 
 // ---------------------------------------------------------------- pool ----
@@ -138,9 +151,10 @@ struct Reader {
 
 template <int K, int MODE>
 struct TState {
-    static constexpr int NW = K / 16;  // 2-bit window words
-    static constexpr int NB = K / 4;   // byte window words (table mode)
-    static constexpr int NM = K / 32;  // liveness mask words
+    static constexpr int WK = (K + 15) / 16 * 16;  // symbol-window slots (multiple of 16)
+    static constexpr int NW = WK / 16;             // 2-bit window words
+    static constexpr int NB = WK / 4;              // byte window words (table mode)
+    static constexpr int NM = (K + 31) / 32;       // liveness mask words
     // unit
     int64_t h_pos, v_pos;
     int32_t m, n, hdir, vdir, unit;

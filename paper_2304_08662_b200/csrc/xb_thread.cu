@@ -1,0 +1,515 @@
+// Thread tiers: one unit per thread, the restricted band of K folded
+// diagonals held in registers (K = 16, 24, 32, 48, 64).  Exact reference
+// semantics (proj/src/align.cpp:37-155); see xb_kernels.cuh for the
+// coordinate system, the drift-space values and the exact running-best chain.
+//
+// Per slot and antidiagonal the kernel issues 8 instructions split evenly
+// over the two integer pipes (B200 ALU pipe and FMA pipe, 16 lanes/clk per
+// SMSP each):
+//   ALU: LOP3 (match bits), VIMNMX3 (recurrence), VIADDMNMX (running best),
+//        ISETP (drop test)
+//   FMA: IMAD.HI (diag + sim), IMAD (slot key), @p IMAD (kill), @p IMAD (dead mask)
+#include <climits>
+#include <cstdint>
+#include <utility>
+
+#include "xb_kernels.cuh"
+
+namespace xb {
+
+__device__ __forceinline__ uint32_t range_bits(int lo, int hi) {
+    if (lo > hi) return 0u;
+    return (0xFFFFFFFFu >> (31 - hi)) & (0xFFFFFFFFu << lo);
+}
+
+template <int K>
+__device__ __forceinline__ void shift_slots(int32_t (&R)[K], int s) {
+    // new slot k <- old slot k + s, vacated slots dead
+    for (; s > 0; --s) {
+#pragma unroll
+        for (int k = 0; k < K - 1; ++k) R[k] = R[k + 1];
+        R[K - 1] = kDeadS;
+    }
+    for (; s < 0; ++s) {
+#pragma unroll
+        for (int k = K - 1; k > 0; --k) R[k] = R[k - 1];
+        R[0] = kDeadS;
+    }
+}
+
+template <int K, int MODE>
+__device__ __forceinline__ void init_windows(TState<K, MODE>& S, const uint32_t* __restrict__ pool) {
+    using St = TState<K, MODE>;
+    const int fd = S.d >> 1, cd = S.d - fd;
+    const int64_t a = int64_t(fd) - S.ubase - 1;  // v index of slot 0
+    const int64_t b = int64_t(cd) + S.ubase - 1;  // h index of slot 0
+    if constexpr (MODE == 0) {
+#pragma unroll
+        for (int w = 0; w < St::NW; ++w) {
+            S.HW[w] = chunk_bf(pool, S.h_pos, S.hdir, b + 16 * w);
+            S.VW[w] = chunk_tf(pool, S.v_pos, S.vdir, a - 16 * w - 15);
+        }
+        S.rv.init(pool, S.v_pos, S.vdir, a + 1);
+        S.rh.init(pool, S.h_pos, S.hdir, b + St::WK);
+    } else {
+        constexpr int ENC = MODE == 1 ? ENC_2BIT : ENC_5BIT;
+#pragma unroll
+        for (int r = 0; r < St::NB; ++r) {
+            uint32_t vw = 0, hw = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int k = 4 * r + q;
+                vw |= code_at<ENC>(pool, S.v_pos, S.vdir, S.n, a - k) << (8 * q);
+                hw |= code_at<ENC>(pool, S.h_pos, S.hdir, S.m, b + k) << (8 * q);
+            }
+            S.VW[r] = vw;
+            S.HW[r] = hw;
+        }
+    }
+}
+
+template <int K, int MODE>
+__device__ __forceinline__ void start_unit(TState<K, MODE>& S, int32_t (&E)[K], int32_t (&O)[K],
+                                           const TierParams& P, uint32_t unit, int32_t X) {
+    const DevUnit u = P.units[unit];
+    S.unit = int32_t(unit);
+    S.h_pos = u.h_pos;
+    S.v_pos = u.v_pos;
+    S.m = u.h_len;
+    S.n = u.v_len;
+    S.hdir = u.dir & 1;
+    S.vdir = (u.dir >> 1) & 1;
+    S.d = 1;
+    S.ubase = -(K / 2);
+    S.fl1 = 0;  // antidiagonal 0: the origin
+    S.ll1 = 0;
+    S.fl2 = 0;  // antidiagonal -1: empty
+    S.ll2 = -1;
+    S.T = 0;
+    S.best_d = 0;
+    S.best_i = 0;
+    S.delta_w = 1;
+    S.cells = 1;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        O[k] = kDeadS;
+        E[k] = (k == K / 2) ? X + 1 : kDeadS;  // s(0,0) = 0 + 0 + off
+    }
+    init_windows(S, P.pool);
+}
+
+// ---- one slot -------------------------------------------------------------
+
+struct SlotCtx {
+    int32_t c;        // running chain value
+    int32_t negC;     // -(64X + 63)
+    int32_t r64, one, zero;
+};
+
+__device__ __forceinline__ int32_t imad_hi(uint32_t a, uint32_t b, int32_t c) {
+    int32_t r;
+    asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
+__device__ __forceinline__ int32_t imad(int32_t a, int32_t b, int32_t c) {
+    int32_t r;
+    asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
+
+// Finishes a slot given its diagonal candidate db and gap sources ln/un:
+// recurrence, key, running best, drop test, dead mask.
+template <int k>
+__device__ __forceinline__ int32_t slot_tail(int32_t db, int32_t ln, int32_t un, SlotCtx& X,
+                                             uint32_t& dm) {
+    int32_t cand = __vimax3_s32(db, ln, un);
+    int32_t key;
+    asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(key) : "r"(cand), "r"(X.r64), "n"(k));
+    X.c = __viaddmax_s32(key, X.negC, X.c);
+    asm("{\n\t.reg .pred p;\n\t"
+        "setp.lt.s32 p, %2, %3;\n\t"
+        "@p mad.lo.s32 %0, %0, %4, %6;\n\t"
+        "@p mad.lo.u32 %1, %5, %7, %1;\n\t}"
+        : "+r"(cand), "+r"(dm)
+        : "r"(key), "r"(X.c), "r"(X.zero), "r"(X.one), "n"(kDeadS), "n"(1u << (k & 31)));
+    return cand;
+}
+
+template <int K, int MODE, bool ODD, int k>
+__device__ __forceinline__ void slot(int32_t (&cur)[K], const int32_t (&prv)[K],
+                                     const uint32_t (&Z)[(K + 15) / 16],
+                                     const TState<K, MODE>& S, const TierParams& P,
+                                     const int8_t* __restrict__ tab, SlotCtx& X,
+                                     uint32_t (&dm)[(K + 31) / 32]) {
+    const int32_t dg = cur[k];
+    int32_t db;
+    if constexpr (MODE == 0) {
+        constexpr int w = k >> 4, f = k & 15;
+        // t = [match bit at 2f+1][1 at 2f]  ->  (t >> 2f) = 1 + 2*match = sim - 2*gap
+        const uint32_t t = (3u << (2 * f)) & Z[w];
+        if constexpr (f == 0)
+            db = imad(int32_t(t), X.one, dg);
+        else
+            db = imad_hi(t, P.mulc[f], dg);
+    } else {
+        constexpr int r = k >> 2, q = k & 3;
+        // bytes: v code, h code, 0, 0 (sign-replicate of a code byte < 128)
+        uint32_t idx;
+        asm("prmt.b32 %0, %1, %2, %3;"
+            : "=r"(idx) : "r"(S.VW[r]), "r"(S.HW[r]), "n"(q | ((q + 4) << 4) | ((8 | q) << 8) | ((8 | q) << 12)));
+        db = imad(int32_t(tab[idx]), X.one, dg);
+    }
+    int32_t ln, un;
+    if constexpr (ODD) {  // gap sources at u and u+1
+        ln = prv[k];
+        un = (k < K - 1) ? prv[k < K - 1 ? k + 1 : k] : kDeadS;
+    } else {              // gap sources at u-1 and u
+        ln = (k > 0) ? prv[k > 0 ? k - 1 : k] : kDeadS;
+        un = prv[k];
+    }
+    cur[k] = slot_tail<k>(db, ln, un, X, dm[k >> 5]);
+}
+
+template <int K, int MODE, bool ODD, int... ks>
+__device__ __forceinline__ void all_slots(std::integer_sequence<int, ks...>, int32_t (&cur)[K],
+                                          const int32_t (&prv)[K], const uint32_t (&Z)[(K + 15) / 16],
+                                          const TState<K, MODE>& S, const TierParams& P,
+                                          const int8_t* __restrict__ tab, SlotCtx& X,
+                                          uint32_t (&dm)[(K + 31) / 32]) {
+    // descending slot = ascending i: the order of the reference's running best
+    (slot<K, MODE, ODD, K - 1 - ks>(cur, prv, Z, S, P, tab, X, dm), ...);
+}
+
+// One antidiagonal d.  cur holds d-2 on entry and d on exit, prv holds d-1.
+template <int K, int MODE, bool ODD>
+__device__ __forceinline__ int xstep(TState<K, MODE>& S, int32_t (&cur)[K], int32_t (&prv)[K],
+                                     const TierParams& P, const int8_t* __restrict__ tab,
+                                     int32_t gap, int32_t X, int32_t& spread) {
+    using St = TState<K, MODE>;
+    const int d = S.d;
+    if (d > S.n + S.m + 1) return kDone;
+    const bool have1 = S.fl1 <= S.ll1, have2 = S.fl2 <= S.ll2;
+    if (!have1 && !have2) return kDone;  // align.cpp:64-66
+
+    // reachable window (align.cpp:68-81)
+    int lo_u = have1 ? S.fl1 : INT_MAX;
+    int hi_u = have1 ? S.ll1 + 1 : INT_MIN;
+    if (have2) {
+        lo_u = min(lo_u, S.fl2 + 1);
+        hi_u = max(hi_u, S.ll2 + 1);
+    }
+    const int lo = max(lo_u, max(d - S.m, 0));
+    const int hi = min(hi_u, min(d, S.n));
+    if (lo <= hi) {  // an empty window counts nothing (align.cpp:84-91)
+        const int w = hi - lo + 1;
+        if (w > P.band) {  // align.cpp:93-94: first overflow, cells so far
+            spread = w;
+            return kBand;
+        }
+        S.cells += w;
+        S.delta_w = max(S.delta_w, w);
+    }
+
+    const int fd = d >> 1, cd = d - fd;
+    // every live source lies inside the unclamped window, so it must fit
+    {
+        const int s_lo = fd - hi_u - S.ubase, s_hi = fd - lo_u - S.ubase;
+        if (s_lo < 0 || s_hi > K - 1) {
+            const int wu = hi_u - lo_u + 1;
+            if (wu > K) return kEscalate;
+            const int nb = fd - hi_u - ((K - wu) >> 1);
+            shift_slots<K>(cur, nb - S.ubase);
+            shift_slots<K>(prv, nb - S.ubase);
+            S.ubase = nb;
+            init_windows(S, P.pool);
+        }
+    }
+
+    // slots inside the matrix: i <= n  <=>  k >= klo ;  j <= m  <=>  k <= khi
+    const int klo = fd - S.ubase - S.n;
+    const int khi = S.m - cd - S.ubase;
+    uint32_t vm[St::NM];
+    [[maybe_unused]] uint32_t vms[St::NW];
+    if (klo <= 0 && khi >= K - 1) {
+#pragma unroll
+        for (int q = 0; q < St::NM; ++q) vm[q] = range_bits(0, min(K - 1 - 32 * q, 31));
+        if constexpr (MODE == 0) {
+#pragma unroll
+            for (int w = 0; w < St::NW; ++w) vms[w] = 0xAAAAAAAAu;
+        }
+    } else {
+        const int khk = min(khi, K - 1);
+#pragma unroll
+        for (int q = 0; q < St::NM; ++q) vm[q] = range_bits(max(klo - 32 * q, 0), min(khk - 32 * q, 31));
+        if constexpr (MODE == 0) {
+#pragma unroll
+            for (int w = 0; w < St::NW; ++w) {
+                const int l = max(klo - 16 * w, 0), h = min(khi - 16 * w, 15);
+                vms[w] = range_bits(2 * l, 2 * h + 1) & 0xAAAAAAAAu;
+            }
+        }
+    }
+
+    // DNA +1/-1/-1: Z[w] bit 2f+1 = slot 16w+f is a match inside the matrix,
+    // bit 2f = 1 (PAT), so one LOP3 per slot isolates [match][1]
+    uint32_t Z[St::NW];
+    if constexpr (MODE == 0) {
+#pragma unroll
+        for (int w = 0; w < St::NW; ++w) {
+            const uint32_t x = S.VW[w] ^ S.HW[w];
+            Z[w] = (~(x | (x << 1)) & vms[w]) | P.pat;
+        }
+    }
+
+    // exact running best + drop test: chain over k = K-1..0 (ascending i)
+    const int32_t beta = -gap;
+    SlotCtx C;
+    C.c = (S.T + beta * d + 1) << 6;  // (T + beta d + off - X) * 64
+    C.negC = -((X << 6) + 63);
+    C.r64 = P.r64;
+    C.one = P.one;
+    C.zero = P.zero;
+    uint32_t dm[St::NM];
+#pragma unroll
+    for (int q = 0; q < St::NM; ++q) dm[q] = 0u;
+    all_slots<K, MODE, ODD>(std::make_integer_sequence<int, K>{}, cur, prv, Z, S, P, tab, C, dm);
+
+    // running best (align.cpp:123-127): strict improvement, first slot wins
+    {
+        const int32_t cf = C.c + ((X << 6) + 63);
+        const int32_t qnew = cf >> 6;
+        const int32_t qold = S.T + beta * d + X + 1;
+        if (qnew > qold) {
+            S.T = qnew - beta * d - X - 1;
+            S.best_d = d;
+            S.best_i = fd - S.ubase - (cf & 63);
+        }
+    }
+    // live range of row d (align.cpp:138-145); out-of-matrix slots masked
+    {
+        uint32_t lv[St::NM];
+        bool any = false;
+#pragma unroll
+        for (int q = 0; q < St::NM; ++q) {
+            lv[q] = ~dm[q] & vm[q];
+            any |= lv[q] != 0u;
+        }
+        S.fl2 = S.fl1;
+        S.ll2 = S.ll1;
+        if (!any) {
+            S.fl1 = 0;
+            S.ll1 = -1;
+        } else {
+            int hs, ls;
+            if constexpr (St::NM == 1) {
+                hs = 31 - __clz(lv[0]);
+                ls = __ffs(lv[0]) - 1;
+            } else {
+                hs = lv[1] ? 63 - __clz(lv[1]) : 31 - __clz(lv[0]);
+                ls = lv[0] ? __ffs(lv[0]) - 1 : 31 + __ffs(lv[1]);
+            }
+            S.fl1 = fd - S.ubase - hs;
+            S.ll1 = fd - S.ubase - ls;
+        }
+    }
+
+    // feed the symbol that enters the band on d+1
+    if constexpr (ODD) {  // floor((d+1)/2) grows: v[a+1] enters at slot 0
+        if constexpr (MODE == 0) {
+#pragma unroll
+            for (int w = St::NW - 1; w > 0; --w) S.VW[w] = __funnelshift_l(S.VW[w - 1], S.VW[w], 2);
+            S.VW[0] = __funnelshift_l(S.rv.cur, S.VW[0], 2);
+            S.rv.cur <<= 2;
+            if (--S.rv.cnt == 0) S.rv.refill(P.pool);
+        } else {
+            constexpr int ENC = MODE == 1 ? ENC_2BIT : ENC_5BIT;
+            const uint32_t code = code_at<ENC>(P.pool, S.v_pos, S.vdir, S.n, int64_t(fd) - S.ubase);
+#pragma unroll
+            for (int r = St::NB - 1; r > 0; --r) S.VW[r] = __funnelshift_l(S.VW[r - 1], S.VW[r], 8);
+            S.VW[0] = (S.VW[0] << 8) | code;
+        }
+    } else {  // ceil((d+1)/2) grows: h[b+WK] enters at slot WK-1
+        if constexpr (MODE == 0) {
+#pragma unroll
+            for (int w = 0; w < St::NW - 1; ++w) S.HW[w] = __funnelshift_r(S.HW[w], S.HW[w + 1], 2);
+            S.HW[St::NW - 1] = __funnelshift_r(S.HW[St::NW - 1], S.rh.cur, 2);
+            S.rh.cur >>= 2;
+            if (--S.rh.cnt == 0) S.rh.refill(P.pool);
+        } else {
+            constexpr int ENC = MODE == 1 ? ENC_2BIT : ENC_5BIT;
+            const uint32_t code =
+                code_at<ENC>(P.pool, S.h_pos, S.hdir, S.m, int64_t(cd) + S.ubase - 1 + St::WK);
+#pragma unroll
+            for (int r = 0; r < St::NB - 1; ++r) S.HW[r] = __funnelshift_r(S.HW[r], S.HW[r + 1], 8);
+            S.HW[St::NB - 1] = __funnelshift_r(S.HW[St::NB - 1], code, 8);
+        }
+    }
+    S.d = d + 1;
+    return kGo;
+}
+
+// Work source of a launch.  Pilot: order[pilot_lo, pilot_hi).  Cascade: the
+// start tier takes the main queue (order minus the pilot sample), each wider
+// tier takes the units escalated into it.
+struct Queue {
+    const uint32_t* q = nullptr;
+    unsigned long long len = 0;
+    unsigned long long* cursor = nullptr;
+    long long skip_lo = 0, skip_n = 0;  // hole to skip in the main queue
+    __device__ __forceinline__ bool next(uint32_t& unit) {
+        const unsigned long long i = atomicAdd(cursor, 1ull);
+        if (i >= len) return false;
+        long long j = (long long)i;
+        if (j >= skip_lo) j += skip_n;
+        unit = q[j];
+        return true;
+    }
+};
+
+__device__ __forceinline__ bool make_queue(const TierParams& P, Queue& Q) {
+    if (P.pilot) {
+        Q.q = P.order + P.pilot_lo;
+        Q.len = (unsigned long long)(P.pilot_hi - P.pilot_lo);
+        Q.cursor = &P.ctr->cursor[7];
+        return true;
+    }
+    const int t0 = P.ctr->start_tier;
+    if (P.tier < t0) return false;
+    Q.cursor = &P.ctr->cursor[P.tier];
+    if (P.tier == t0) {
+        Q.q = P.order;
+        Q.len = (unsigned long long)(P.n_units - (P.pilot_hi - P.pilot_lo));
+        Q.skip_lo = P.pilot_lo;
+        Q.skip_n = P.pilot_hi - P.pilot_lo;
+    } else {
+        Q.q = P.lists + (long long)P.tier * P.n_units;
+        Q.len = P.ctr->list_len[P.tier];
+    }
+    return true;
+}
+
+template <int K, int MODE>
+__global__ void __launch_bounds__(kTB) thread_tier_kernel(TierParams P) {
+    __shared__ int8_t tab[MODE == 0 ? 4 : 32 * 256];
+    const int32_t gap = P.scheme->gap, X = P.scheme->x;
+    Queue Q;
+    if (!make_queue(P, Q)) return;
+    if constexpr (MODE != 0) {
+        // tab[h*256 + v] = sim(v, h) - 2*gap; sentinel rows/cols lose
+        for (int q = threadIdx.x; q < 32 * 256; q += blockDim.x) {
+            const int h = q >> 8, v = q & 255;
+            int val = -128;
+            if (v < 32 && h != kSentinel && v != kSentinel) {
+                val = P.scheme->sim[v * 32 + h] - 2 * gap;
+                val = max(-127, min(127, val));
+            }
+            tab[q] = int8_t(val);
+        }
+        __syncthreads();
+    }
+    const int next_tier = P.tier + 1;
+    uint32_t* esc_list = P.lists + (long long)next_tier * P.n_units;
+    unsigned long long* esc_len = &P.ctr->list_len[next_tier];
+    unsigned long long my_units = 0, my_cells = 0, my_esc = 0;
+
+    TState<K, MODE> S;
+    int32_t E[K], O[K];
+    bool active = false;
+    auto fetch = [&]() {
+        active = false;
+        uint32_t unit;
+        while (Q.next(unit)) {
+            // units whose values could leave the drift-space range go to the warp tier
+            if (P.units[unit].route != 0) continue;
+            start_unit<K, MODE>(S, E, O, P, unit, X);
+            active = true;
+            return;
+        }
+    };
+    fetch();
+
+    while (__any_sync(0xFFFFFFFFu, active)) {
+        if (active) {
+            int32_t spread = 0;
+            int r = xstep<K, MODE, true>(S, O, E, P, tab, gap, X, spread);
+            if (r == kGo) r = xstep<K, MODE, false>(S, E, O, P, tab, gap, X, spread);
+            if (r != kGo) {
+                DevResult res;
+                res.cells = S.cells;
+                res.delta_w = S.delta_w;
+                res.spread = 0;
+                if (r == kEscalate) {
+                    const unsigned long long slot = atomicAdd(esc_len, 1ull);
+                    esc_list[slot] = uint32_t(S.unit);
+                    ++my_esc;
+                    res.score = res.h_ext = res.v_ext = 0;
+                    res.status = kStatusEscalated;  // overwritten by the wider tier
+                    res.spread = K + 1;
+                } else {
+                    if (r == kBand) {
+                        res.score = res.h_ext = res.v_ext = 0;
+                        res.status = kStatusBand;
+                        res.spread = spread;
+                    } else {
+                        res.score = S.T;
+                        res.h_ext = S.best_d - S.best_i;
+                        res.v_ext = S.best_i;
+                        res.status = kStatusOk;
+                    }
+                    ++my_units;
+                    my_cells += (unsigned long long)S.cells;
+                }
+                P.results[S.unit] = res;
+                fetch();
+            }
+        }
+    }
+    const int st = P.tier;  // pilot work is accounted to its own (K=64) tier
+    if (my_units) atomicAdd(&P.ctr->units[st], my_units);
+    if (my_cells) atomicAdd(&P.ctr->cells[st], my_cells);
+    if (my_esc) atomicAdd(&P.ctr->escalated[st], my_esc);
+}
+
+#define XB_INST(K)                                                   \
+    template __global__ void thread_tier_kernel<K, 0>(TierParams);   \
+    template __global__ void thread_tier_kernel<K, 1>(TierParams);   \
+    template __global__ void thread_tier_kernel<K, 2>(TierParams);
+XB_INST(16)
+XB_INST(24)
+XB_INST(32)
+XB_INST(48)
+XB_INST(64)
+#undef XB_INST
+
+// Picks the start tier from the pilot sample: the width that minimises
+// K_t + sum over wider tiers of (share escalating into them) * 1.5 * K.
+__global__ void select_tier_kernel(TierParams P, int forced) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (forced >= 0) {
+        P.ctr->start_tier = forced;
+        return;
+    }
+    long long need[6] = {0, 0, 0, 0, 0, 0};  // units needing more than tier t
+    long long n = 0;
+    for (long long q = P.pilot_lo; q < P.pilot_hi; ++q) {
+        const uint32_t u = P.order[q];
+        if (P.units[u].route != 0) continue;
+        const DevResult r = P.results[u];
+        const int w = r.status == kStatusEscalated ? (1 << 30) : r.delta_w + 2;  // +2: unclamped slack
+        ++n;
+        for (int t = 0; t < 5; ++t) need[t] += w > tier_width(t) && P.band > tier_width(t);
+    }
+    int best = 4;
+    double best_cost = 1e30;
+    for (int t = 0; t < 5; ++t) {
+        double cost = tier_width(t);
+        for (int u = t + 1; u < 5; ++u) cost += 1.5 * tier_width(u) * (n ? double(need[u - 1]) / n : 0.0);
+        if (cost < best_cost) {
+            best_cost = cost;
+            best = t;
+        }
+    }
+    P.ctr->start_tier = best;
+}
+
+}  // namespace xb

@@ -35,7 +35,8 @@ st = capi.XbStats()
 L.xb_batch_stats(b, C.byref(st))
 d = st.as_dict()
 cells = sum(d["cells_tier"])
-print(f"config {a.config} x{a.scale}: {len(t)} tasks, {cells} cells, tiers ms {d['ms_tier']}, "
-      f"units {d['units_tier']}, escalated {d['escalated']}, prep {d['ms_prep']:.2f} ms, "
+print(f"config {a.config} x{a.scale}: {len(t)} tasks, {cells} cells, start tier {d['start_tier']}, "
+      f"tiers ms {[round(x, 3) for x in d['ms_tier']]}, units {d['units_tier']}, escalated {d['escalated']}, "
+      f"prep {d['ms_prep']:.2f} ms, pilot {d['ms_pilot']:.2f} ms, "
       f"GCUPS {cells / (d['ms_total'] / 1e3) / 1e9:.1f}")
 L.xb_batch_free(b)

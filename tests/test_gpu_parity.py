@@ -54,7 +54,11 @@ def _by_scheme(entries):
     return groups
 
 
-@pytest.mark.parametrize("flags", [0, 2, 4], ids=["cascade", "warp_tier_only", "tier64_first"])
+TIER_FLAGS = [0, 2] + [8 | (t << 8) for t in range(5)]
+TIER_IDS = ["pilot_cascade", "warp_tier_only", "k16", "k24", "k32", "k48", "k64"]
+
+
+@pytest.mark.parametrize("flags", TIER_FLAGS, ids=TIER_IDS)
 def test_vectors_all_tiers(xb, flags):
     entries = VEC["kats"] + VEC["random"]
     bad = []
@@ -130,7 +134,8 @@ def _config_pool(xb, ds):
 
 
 @pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
-@pytest.mark.parametrize("flags", [0, 1, 2], ids=["cascade", "unsorted", "warp_tier_only"])
+@pytest.mark.parametrize("flags", [0, 1, 2, 8 | (0 << 8), 8 | (2 << 8)],
+                         ids=["cascade", "unsorted", "warp_tier_only", "from_k16", "from_k32"])
 def test_configs_vs_reference_golden(xb, cfg, flags):
     from paper_2304_08662_b200 import synth
     meta = load_json("configs_meta.json")[str(cfg)]
