@@ -31,6 +31,7 @@ XB_SIDE_BAND_EXCEEDED = 1
 XB_FLAG_NO_SORT = 1
 XB_FLAG_GENERIC_ONLY = 2
 XB_FLAG_FORCE_TIER = 8
+XB_FLAG_ESC_TO_WARP = 16
 
 
 def force_tier(t: int) -> int:

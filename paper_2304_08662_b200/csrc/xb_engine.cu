@@ -476,6 +476,7 @@ struct DevBatch {
     uint32_t* d_lists = nullptr;  // kNumTiers x n_units escalation inputs
     DevCounters* d_ctr = nullptr;
     int32_t* d_scratch = nullptr;
+    int32_t* d_pilot = nullptr;
     int scratch_warps = 0;
     void* d_cub = nullptr;
     size_t cub_bytes = 0;
@@ -514,6 +515,7 @@ static void free_dev(DevBatch& D) {
     cudaFree(D.d_lists);
     cudaFree(D.d_ctr);
     cudaFree(D.d_scratch);
+    cudaFree(D.d_pilot);
     cudaFree(D.d_cub);
     for (auto& e : D.ev)
         if (e) cudaEventDestroy(e);
@@ -551,6 +553,7 @@ static int setup_device(xb_batch* B, DevBatch& D, const xb_exec* ex) {
     CK(cudaMalloc(&D.d_res, U * sizeof(DevResult)));
     CK(cudaMalloc(&D.d_lists, U * 4 * kNumTiers));
     CK(cudaMalloc(&D.d_ctr, sizeof(DevCounters)));
+    CK(cudaMalloc(&D.d_pilot, (U / 512 + 128) * 4));
     CK(cudaMallocHost(&D.h_res, U * sizeof(DevResult)));
     if (!B->units_mode) {
         CK(cudaMalloc(&D.d_tasks, size_t(std::max<int64_t>(D.n_items, 1)) * 32));
@@ -724,16 +727,19 @@ static int run_device(xb_batch* B, DevBatch& D) {
     tp.one = 1;
     tp.zero = 0;
     for (int f = 0; f < 16; ++f) tp.mulc[f] = f ? (1u << (32 - 2 * f)) : 0u;
-    // pilot sample: the middle of the longest-first order (unbiased widths,
-    // short enough not to stall the machine)
+    // pilot: a strided sample of the order, each unit run for at most
+    // kPilotCap antidiagonals on the widest thread tier, to measure widths
     const int forced = (B->flags & XB_FLAG_FORCE_TIER) ? ((B->flags >> 8) & 15) : -1;
-    long long pn = (forced >= 0 || (B->flags & XB_FLAG_GENERIC_ONLY)) ? 0 : std::min<long long>(nu, 64 + nu / 256);
-    tp.pilot_lo = (nu - pn) / 2;
-    tp.pilot_hi = tp.pilot_lo + pn;
+    const long long pn = (forced >= 0 || (B->flags & XB_FLAG_GENERIC_ONLY))
+                             ? 0 : std::min<long long>(nu, 64 + nu / 512);
+    tp.pilot_n = pn;
+    tp.pilot_stride = pn ? std::max<long long>(1, nu / pn) : 1;
+    tp.pilot_cap = 4096;
+    tp.pilot_w = D.d_pilot;
+    tp.esc_to_warp = (B->flags & XB_FLAG_ESC_TO_WARP) ? 1 : 0;
     D.mode = mode;
     for (int t = 0; t < 5; ++t)
         if (!D.occ[t]) CK(occupancy_blocks(t, mode, &D.occ[t]) ? cudaErrorUnknown : cudaSuccess);
-    // ---- pilot on the widest thread tier, then pick the start tier ----
     if (pn > 0) {
         tp.tier = 4;
         tp.pilot = 1;

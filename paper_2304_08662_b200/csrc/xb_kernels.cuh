@@ -35,6 +35,7 @@ namespace xb {
 
 constexpr int32_t kDeadS = -(1 << 24);  // dead sentinel in drift space
 constexpr int kTB = 128;                // threads per block, thread tiers
+constexpr int32_t kBig = 1 << 29;       // empty live range = [kBig, -kBig]
 
 // Thread tiers: band widths K (slots per unit); index 5 is the warp tier.
 constexpr int kNumTiers = 6;
@@ -52,10 +53,13 @@ struct TierParams {
     DevCounters* __restrict__ ctr;
     const DevScheme* __restrict__ scheme;
     long long n_units;
-    long long pilot_lo, pilot_hi;        // order[pilot_lo, pilot_hi) is the pilot sample
+    int32_t* __restrict__ pilot_w;       // pilot: widest window seen per sample (-1: > 64)
+    long long pilot_n, pilot_stride;     // pilot sample = order[q * stride], q < pilot_n
+    int32_t pilot_cap;                   // pilot: antidiagonals run per sample unit
     int32_t band;
     int32_t tier;                        // this launch's tier index
     int32_t pilot;                       // 1: run the pilot sample, 0: cascade
+    int32_t esc_to_warp;                 // escalations skip the wider thread tiers
     int32_t* __restrict__ warp_scratch;  // warp tier: 2*band ints per warp slot
     // opaque constants: kept in c[]/uniform registers so ptxas cannot fold
     // them into ALU-pipe forms (LEA, LOP3 immediates, SEL)
@@ -159,10 +163,10 @@ struct TState {
     int64_t h_pos, v_pos;
     int32_t m, n, hdir, vdir, unit;
     // progress
-    int32_t d, ubase;
-    int32_t fl1, ll1, fl2, ll2;  // live i-ranges of rows d-1 and d-2
+    int32_t d, ubase, dcap;
+    int32_t fl1, ll1, fl2, ll2;  // live i-ranges of rows d-1, d-2; empty = (kBig, -kBig)
     int32_t T, best_d, best_i, delta_w;
-    int64_t cells;
+    int32_t cells;               // <= 64 (n + m + 1): int32 under the prep guard
     // windows
     uint32_t VW[MODE == 0 ? NW : NB];
     uint32_t HW[MODE == 0 ? NW : NB];

@@ -80,11 +80,12 @@ __device__ __forceinline__ void start_unit(TState<K, MODE>& S, int32_t (&E)[K], 
     S.hdir = u.dir & 1;
     S.vdir = (u.dir >> 1) & 1;
     S.d = 1;
+    S.dcap = P.pilot ? P.pilot_cap : INT_MAX;
     S.ubase = -(K / 2);
     S.fl1 = 0;  // antidiagonal 0: the origin
     S.ll1 = 0;
-    S.fl2 = 0;  // antidiagonal -1: empty
-    S.ll2 = -1;
+    S.fl2 = kBig;  // antidiagonal -1: empty
+    S.ll2 = -kBig;
     S.T = 0;
     S.best_d = 0;
     S.best_i = 0;
@@ -148,9 +149,9 @@ __device__ __forceinline__ void slot(int32_t (&cur)[K], const int32_t (&prv)[K],
         // t = [match bit at 2f+1][1 at 2f]  ->  (t >> 2f) = 1 + 2*match = sim - 2*gap
         const uint32_t t = (3u << (2 * f)) & Z[w];
         if constexpr (f == 0)
-            db = imad(int32_t(t), X.one, dg);
+            db = dg + int32_t(t);
         else
-            db = imad_hi(t, P.mulc[f], dg);
+            db = dg + int32_t(__umulhi(t, 1u << (32 - 2 * f)));  // LEA.HI: dg + (t >> 2f)
     } else {
         constexpr int r = k >> 2, q = k & 3;
         // bytes: v code, h code, 0, 0 (sign-replicate of a code byte < 128)
@@ -187,43 +188,34 @@ __device__ __forceinline__ int xstep(TState<K, MODE>& S, int32_t (&cur)[K], int3
                                      int32_t gap, int32_t X, int32_t& spread) {
     using St = TState<K, MODE>;
     const int d = S.d;
-    if (d > S.n + S.m + 1) return kDone;
-    const bool have1 = S.fl1 <= S.ll1, have2 = S.fl2 <= S.ll2;
-    if (!have1 && !have2) return kDone;  // align.cpp:64-66
-
-    // reachable window (align.cpp:68-81)
-    int lo_u = have1 ? S.fl1 : INT_MAX;
-    int hi_u = have1 ? S.ll1 + 1 : INT_MIN;
-    if (have2) {
-        lo_u = min(lo_u, S.fl2 + 1);
-        hi_u = max(hi_u, S.ll2 + 1);
-    }
-    const int lo = max(lo_u, max(d - S.m, 0));
-    const int hi = min(hi_u, min(d, S.n));
-    if (lo <= hi) {  // an empty window counts nothing (align.cpp:84-91)
-        const int w = hi - lo + 1;
+    // reachable window (align.cpp:68-81); an empty row is [kBig, -kBig] so
+    // the min/max need no liveness tests
+    const int lo_u = min(S.fl1, S.fl2 + 1);
+    const int hi_u = max(S.ll1, S.ll2) + 1;
+    const int lo = __vimax3_s32(lo_u, d - S.m, 0);
+    const int hi = __vimin3_s32(hi_u, d, S.n);
+    const int w = hi - lo + 1;  // <= 0: empty window, counts nothing (align.cpp:84-91)
+    const int fd = d >> 1, cd = d - fd;
+    const int s_lo = fd - hi_u - S.ubase, s_hi = fd - lo_u - S.ubase;
+    // one rarely-taken branch for every way a step can stop or reshape
+    if (lo_u >= kBig || d > S.dcap || w > P.band || s_lo < 0 || s_hi > K - 1) {
+        if (lo_u >= kBig || d > S.n + S.m + 1) return kDone;  // align.cpp:64-66
         if (w > P.band) {  // align.cpp:93-94: first overflow, cells so far
             spread = w;
             return kBand;
         }
-        S.cells += w;
-        S.delta_w = max(S.delta_w, w);
+        if (d > S.dcap) return kDone;  // pilot: prefix only
+        // every live source lies inside the unclamped window, so it must fit
+        const int wu = hi_u - lo_u + 1;
+        if (wu > K) return kEscalate;
+        const int nb = fd - hi_u - ((K - wu) >> 1);
+        shift_slots<K>(cur, nb - S.ubase);
+        shift_slots<K>(prv, nb - S.ubase);
+        S.ubase = nb;
+        init_windows(S, P.pool);
     }
-
-    const int fd = d >> 1, cd = d - fd;
-    // every live source lies inside the unclamped window, so it must fit
-    {
-        const int s_lo = fd - hi_u - S.ubase, s_hi = fd - lo_u - S.ubase;
-        if (s_lo < 0 || s_hi > K - 1) {
-            const int wu = hi_u - lo_u + 1;
-            if (wu > K) return kEscalate;
-            const int nb = fd - hi_u - ((K - wu) >> 1);
-            shift_slots<K>(cur, nb - S.ubase);
-            shift_slots<K>(prv, nb - S.ubase);
-            S.ubase = nb;
-            init_windows(S, P.pool);
-        }
-    }
+    S.cells += max(w, 0);
+    S.delta_w = max(S.delta_w, w);
 
     // slots inside the matrix: i <= n  <=>  k >= klo ;  j <= m  <=>  k <= khi
     const int klo = fd - S.ubase - S.n;
@@ -297,8 +289,8 @@ __device__ __forceinline__ int xstep(TState<K, MODE>& S, int32_t (&cur)[K], int3
         S.fl2 = S.fl1;
         S.ll2 = S.ll1;
         if (!any) {
-            S.fl1 = 0;
-            S.ll1 = -1;
+            S.fl1 = kBig;
+            S.ll1 = -kBig;
         } else {
             int hs, ls;
             if constexpr (St::NM == 1) {
@@ -348,28 +340,28 @@ __device__ __forceinline__ int xstep(TState<K, MODE>& S, int32_t (&cur)[K], int3
     return kGo;
 }
 
-// Work source of a launch.  Pilot: order[pilot_lo, pilot_hi).  Cascade: the
-// start tier takes the main queue (order minus the pilot sample), each wider
-// tier takes the units escalated into it.
+// Work source of a launch.  Pilot: a strided sample of the order.  Cascade:
+// the start tier takes the whole main queue, each wider tier the units
+// escalated into it.
 struct Queue {
     const uint32_t* q = nullptr;
     unsigned long long len = 0;
     unsigned long long* cursor = nullptr;
-    long long skip_lo = 0, skip_n = 0;  // hole to skip in the main queue
-    __device__ __forceinline__ bool next(uint32_t& unit) {
+    long long stride = 1;
+    __device__ __forceinline__ bool next(uint32_t& unit, long long& idx) {
         const unsigned long long i = atomicAdd(cursor, 1ull);
         if (i >= len) return false;
-        long long j = (long long)i;
-        if (j >= skip_lo) j += skip_n;
-        unit = q[j];
+        idx = (long long)i;
+        unit = q[(long long)i * stride];
         return true;
     }
 };
 
 __device__ __forceinline__ bool make_queue(const TierParams& P, Queue& Q) {
     if (P.pilot) {
-        Q.q = P.order + P.pilot_lo;
-        Q.len = (unsigned long long)(P.pilot_hi - P.pilot_lo);
+        Q.q = P.order;
+        Q.len = (unsigned long long)P.pilot_n;
+        Q.stride = P.pilot_stride;
         Q.cursor = &P.ctr->cursor[7];
         return true;
     }
@@ -378,9 +370,7 @@ __device__ __forceinline__ bool make_queue(const TierParams& P, Queue& Q) {
     Q.cursor = &P.ctr->cursor[P.tier];
     if (P.tier == t0) {
         Q.q = P.order;
-        Q.len = (unsigned long long)(P.n_units - (P.pilot_hi - P.pilot_lo));
-        Q.skip_lo = P.pilot_lo;
-        Q.skip_n = P.pilot_hi - P.pilot_lo;
+        Q.len = (unsigned long long)P.n_units;
     } else {
         Q.q = P.lists + (long long)P.tier * P.n_units;
         Q.len = P.ctr->list_len[P.tier];
@@ -388,8 +378,12 @@ __device__ __forceinline__ bool make_queue(const TierParams& P, Queue& Q) {
     return true;
 }
 
+// resident blocks per SM the register budget is sized for
+template <int K>
+constexpr int tier_min_blocks() { return K <= 24 ? 4 : K <= 32 ? 3 : 2; }
+
 template <int K, int MODE>
-__global__ void __launch_bounds__(kTB) thread_tier_kernel(TierParams P) {
+__global__ void __launch_bounds__(kTB, tier_min_blocks<K>()) thread_tier_kernel(TierParams P) {
     __shared__ int8_t tab[MODE == 0 ? 4 : 32 * 256];
     const int32_t gap = P.scheme->gap, X = P.scheme->x;
     Queue Q;
@@ -407,7 +401,7 @@ __global__ void __launch_bounds__(kTB) thread_tier_kernel(TierParams P) {
         }
         __syncthreads();
     }
-    const int next_tier = P.tier + 1;
+    const int next_tier = P.esc_to_warp ? kWarpTier : P.tier + 1;
     uint32_t* esc_list = P.lists + (long long)next_tier * P.n_units;
     unsigned long long* esc_len = &P.ctr->list_len[next_tier];
     unsigned long long my_units = 0, my_cells = 0, my_esc = 0;
@@ -415,12 +409,16 @@ __global__ void __launch_bounds__(kTB) thread_tier_kernel(TierParams P) {
     TState<K, MODE> S;
     int32_t E[K], O[K];
     bool active = false;
+    long long qidx = 0;
     auto fetch = [&]() {
         active = false;
         uint32_t unit;
-        while (Q.next(unit)) {
+        while (Q.next(unit, qidx)) {
             // units whose values could leave the drift-space range go to the warp tier
-            if (P.units[unit].route != 0) continue;
+            if (P.units[unit].route != 0) {
+                if (P.pilot) P.pilot_w[qidx] = -2;  // not a thread-tier unit
+                continue;
+            }
             start_unit<K, MODE>(S, E, O, P, unit, X);
             active = true;
             return;
@@ -434,18 +432,16 @@ __global__ void __launch_bounds__(kTB) thread_tier_kernel(TierParams P) {
             int r = xstep<K, MODE, true>(S, O, E, P, tab, gap, X, spread);
             if (r == kGo) r = xstep<K, MODE, false>(S, E, O, P, tab, gap, X, spread);
             if (r != kGo) {
-                DevResult res;
-                res.cells = S.cells;
-                res.delta_w = S.delta_w;
-                res.spread = 0;
-                if (r == kEscalate) {
+                if (P.pilot) {
+                    P.pilot_w[qidx] = r == kEscalate ? -1 : S.delta_w;
+                } else if (r == kEscalate) {
                     const unsigned long long slot = atomicAdd(esc_len, 1ull);
                     esc_list[slot] = uint32_t(S.unit);
                     ++my_esc;
-                    res.score = res.h_ext = res.v_ext = 0;
-                    res.status = kStatusEscalated;  // overwritten by the wider tier
-                    res.spread = K + 1;
                 } else {
+                    DevResult res;
+                    res.cells = S.cells;
+                    res.delta_w = S.delta_w;
                     if (r == kBand) {
                         res.score = res.h_ext = res.v_ext = 0;
                         res.status = kStatusBand;
@@ -455,19 +451,20 @@ __global__ void __launch_bounds__(kTB) thread_tier_kernel(TierParams P) {
                         res.h_ext = S.best_d - S.best_i;
                         res.v_ext = S.best_i;
                         res.status = kStatusOk;
+                        res.spread = 0;
                     }
+                    P.results[S.unit] = res;
                     ++my_units;
                     my_cells += (unsigned long long)S.cells;
                 }
-                P.results[S.unit] = res;
                 fetch();
             }
         }
     }
-    const int st = P.tier;  // pilot work is accounted to its own (K=64) tier
-    if (my_units) atomicAdd(&P.ctr->units[st], my_units);
-    if (my_cells) atomicAdd(&P.ctr->cells[st], my_cells);
-    if (my_esc) atomicAdd(&P.ctr->escalated[st], my_esc);
+    if (P.pilot) return;
+    if (my_units) atomicAdd(&P.ctr->units[P.tier], my_units);
+    if (my_cells) atomicAdd(&P.ctr->cells[P.tier], my_cells);
+    if (my_esc) atomicAdd(&P.ctr->escalated[P.tier], my_esc);
 }
 
 #define XB_INST(K)                                                   \
@@ -489,13 +486,12 @@ __global__ void select_tier_kernel(TierParams P, int forced) {
         P.ctr->start_tier = forced;
         return;
     }
-    long long need[6] = {0, 0, 0, 0, 0, 0};  // units needing more than tier t
+    long long need[6] = {0, 0, 0, 0, 0, 0};  // sample units needing more than tier t
     long long n = 0;
-    for (long long q = P.pilot_lo; q < P.pilot_hi; ++q) {
-        const uint32_t u = P.order[q];
-        if (P.units[u].route != 0) continue;
-        const DevResult r = P.results[u];
-        const int w = r.status == kStatusEscalated ? (1 << 30) : r.delta_w + 2;  // +2: unclamped slack
+    for (long long q = 0; q < P.pilot_n; ++q) {
+        const int pw = P.pilot_w[q];
+        if (pw == -2) continue;
+        const int w = pw < 0 ? (1 << 30) : pw + 2;  // +2: unclamped-window slack
         ++n;
         for (int t = 0; t < 5; ++t) need[t] += w > tier_width(t) && P.band > tier_width(t);
     }
