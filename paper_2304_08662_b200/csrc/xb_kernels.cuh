@@ -110,44 +110,41 @@ __device__ __forceinline__ uint32_t code_at(const uint32_t* __restrict__ pool, i
     return (ldw(pool, int64_t(wi)) >> (uint32_t(up - wi * 6u) * 5u)) & 31u;
 }
 
-// Streams consecutive 16-symbol chunks of a 2-bit view, one new word load per
-// chunk, issued a full chunk ahead of use.  TOP = chunks top-first (v side)
+// Streams consecutive 16-symbol chunks of a 2-bit view.  Refills happen at
+// warp-uniform loop iterations (every 16), so no thread diverges for them:
+// `cur` is filled at (re)initialisation with the symbols needed up to the
+// next refill point, and each refill assembles the chunk whose words were
+// loaded one refill (16 iterations) earlier.  TOP = chunks top-first (v side).
 template <bool TOP>
 struct Reader {
-    uint32_t cur;   // remaining symbols of the current chunk
+    uint32_t cur;   // remaining symbols until the next refill point
     uint32_t w0, w1;
     int64_t wnext;  // word index of the next load
     uint32_t sh;
-    int32_t cnt;
     int32_t dir;
 
-    __device__ __forceinline__ void init(const uint32_t* pool, int64_t pos, int d, int64_t t0) {
+    // t0: view index of the next symbol to consume; r: symbols consumed
+    // before the next refill point
+    __device__ __forceinline__ void init(const uint32_t* pool, int64_t pos, int d, int64_t t0, int r) {
         dir = d;
-        // current chunk at t0, words for chunk t0+16 preloaded
         cur = TOP ? chunk_tf(pool, pos, d, t0) : chunk_bf(pool, pos, d, t0);
-        const int64_t q = d ? pos + t0 + 16 : pos - (t0 + 16) - 15;
+        const int64_t q = d ? pos + t0 + r : pos - (t0 + r) - 15;
         const int64_t wi = q >> 4;
         sh = uint32_t(q & 15) * 2u;
         w0 = ldw(pool, wi);
         w1 = ldw(pool, wi + 1);
         wnext = d ? wi + 2 : wi - 1;
-        cnt = 16;
     }
     __device__ __forceinline__ void refill(const uint32_t* pool) {
-        uint32_t c = __funnelshift_r(w0, w1, sh);
+        const uint32_t c = __funnelshift_r(w0, w1, sh);
         const bool rev = TOP ? (dir != 0) : (dir == 0);
         cur = rev ? rev16(c) : c;
         const uint32_t nw = ldw(pool, wnext);
-        if (dir) {
-            w0 = w1;
-            w1 = nw;
-            wnext += 1;
-        } else {
-            w1 = w0;
-            w0 = nw;
-            wnext -= 1;
-        }
-        cnt = 16;
+        const bool fwd = dir != 0;
+        const uint32_t o0 = w0, o1 = w1;
+        w0 = fwd ? o1 : nw;
+        w1 = fwd ? nw : o0;
+        wnext += fwd ? 1 : -1;
     }
 };
 

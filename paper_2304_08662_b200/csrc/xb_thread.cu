@@ -37,8 +37,10 @@ __device__ __forceinline__ void shift_slots(int32_t (&R)[K], int s) {
     }
 }
 
+// rv_r / rh_r: symbols each reader consumes before the next refill point
 template <int K, int MODE>
-__device__ __forceinline__ void init_windows(TState<K, MODE>& S, const uint32_t* __restrict__ pool) {
+__device__ __forceinline__ void init_windows(TState<K, MODE>& S, const uint32_t* __restrict__ pool,
+                                             int rv_r, int rh_r) {
     using St = TState<K, MODE>;
     const int fd = S.d >> 1, cd = S.d - fd;
     const int64_t a = int64_t(fd) - S.ubase - 1;  // v index of slot 0
@@ -49,8 +51,8 @@ __device__ __forceinline__ void init_windows(TState<K, MODE>& S, const uint32_t*
             S.HW[w] = chunk_bf(pool, S.h_pos, S.hdir, b + 16 * w);
             S.VW[w] = chunk_tf(pool, S.v_pos, S.vdir, a - 16 * w - 15);
         }
-        S.rv.init(pool, S.v_pos, S.vdir, a + 1);
-        S.rh.init(pool, S.h_pos, S.hdir, b + St::WK);
+        S.rv.init(pool, S.v_pos, S.vdir, a + 1, rv_r);
+        S.rh.init(pool, S.h_pos, S.hdir, b + St::WK, rh_r);
     } else {
         constexpr int ENC = MODE == 1 ? ENC_2BIT : ENC_5BIT;
 #pragma unroll
@@ -70,7 +72,7 @@ __device__ __forceinline__ void init_windows(TState<K, MODE>& S, const uint32_t*
 
 template <int K, int MODE>
 __device__ __forceinline__ void start_unit(TState<K, MODE>& S, int32_t (&E)[K], int32_t (&O)[K],
-                                           const TierParams& P, uint32_t unit, int32_t X) {
+                                           const TierParams& P, uint32_t unit, int32_t X, unsigned it) {
     const DevUnit u = P.units[unit];
     S.unit = int32_t(unit);
     S.h_pos = u.h_pos;
@@ -96,7 +98,9 @@ __device__ __forceinline__ void start_unit(TState<K, MODE>& S, int32_t (&E)[K], 
         O[k] = kDeadS;
         E[k] = (k == K / 2) ? X + 1 : kDeadS;  // s(0,0) = 0 + 0 + off
     }
-    init_windows(S, P.pool);
+    // started at the end of iteration it: consumption begins next iteration
+    const int r = 15 - int(it & 15);
+    init_windows(S, P.pool, r, r);
 }
 
 // ---- one slot -------------------------------------------------------------
@@ -185,7 +189,7 @@ __device__ __forceinline__ void all_slots(std::integer_sequence<int, ks...>, int
 template <int K, int MODE, bool ODD>
 __device__ __forceinline__ int xstep(TState<K, MODE>& S, int32_t (&cur)[K], int32_t (&prv)[K],
                                      const TierParams& P, const int8_t* __restrict__ tab,
-                                     int32_t gap, int32_t X, int32_t& spread) {
+                                     int32_t gap, int32_t X, int32_t& spread, unsigned it) {
     using St = TState<K, MODE>;
     const int d = S.d;
     // reachable window (align.cpp:68-81); an empty row is [kBig, -kBig] so
@@ -212,7 +216,10 @@ __device__ __forceinline__ int xstep(TState<K, MODE>& S, int32_t (&cur)[K], int3
         shift_slots<K>(cur, nb - S.ubase);
         shift_slots<K>(prv, nb - S.ubase);
         S.ubase = nb;
-        init_windows(S, P.pool);
+        // symbols left to consume before the next refill (iteration multiple of 16):
+        // this iteration's own consumption counts unless it already happened
+        const int to_refill = 16 - int(it & 15);
+        init_windows(S, P.pool, ODD ? to_refill : to_refill - 1, to_refill);
     }
     S.cells += max(w, 0);
     S.delta_w = max(S.delta_w, w);
@@ -279,30 +286,24 @@ __device__ __forceinline__ int xstep(TState<K, MODE>& S, int32_t (&cur)[K], int3
     }
     // live range of row d (align.cpp:138-145); out-of-matrix slots masked
     {
-        uint32_t lv[St::NM];
-        bool any = false;
-#pragma unroll
-        for (int q = 0; q < St::NM; ++q) {
-            lv[q] = ~dm[q] & vm[q];
-            any |= lv[q] != 0u;
+        int hs, ls;
+        bool any;
+        if constexpr (St::NM == 1) {
+            const uint32_t lv = ~dm[0] & vm[0];
+            any = lv != 0u;
+            hs = 31 - __clz(lv);
+            ls = __ffs(lv) - 1;
+        } else {
+            const uint32_t lv0 = ~dm[0] & vm[0], lv1 = ~dm[1] & vm[1];
+            any = (lv0 | lv1) != 0u;
+            hs = lv1 ? 63 - __clz(lv1) : 31 - __clz(lv0);
+            ls = lv0 ? __ffs(lv0) - 1 : 31 + __ffs(lv1);
         }
         S.fl2 = S.fl1;
         S.ll2 = S.ll1;
-        if (!any) {
-            S.fl1 = kBig;
-            S.ll1 = -kBig;
-        } else {
-            int hs, ls;
-            if constexpr (St::NM == 1) {
-                hs = 31 - __clz(lv[0]);
-                ls = __ffs(lv[0]) - 1;
-            } else {
-                hs = lv[1] ? 63 - __clz(lv[1]) : 31 - __clz(lv[0]);
-                ls = lv[0] ? __ffs(lv[0]) - 1 : 31 + __ffs(lv[1]);
-            }
-            S.fl1 = fd - S.ubase - hs;
-            S.ll1 = fd - S.ubase - ls;
-        }
+        const int base = fd - S.ubase;
+        S.fl1 = any ? base - hs : kBig;
+        S.ll1 = any ? base - ls : -kBig;
     }
 
     // feed the symbol that enters the band on d+1
@@ -312,7 +313,6 @@ __device__ __forceinline__ int xstep(TState<K, MODE>& S, int32_t (&cur)[K], int3
             for (int w = St::NW - 1; w > 0; --w) S.VW[w] = __funnelshift_l(S.VW[w - 1], S.VW[w], 2);
             S.VW[0] = __funnelshift_l(S.rv.cur, S.VW[0], 2);
             S.rv.cur <<= 2;
-            if (--S.rv.cnt == 0) S.rv.refill(P.pool);
         } else {
             constexpr int ENC = MODE == 1 ? ENC_2BIT : ENC_5BIT;
             const uint32_t code = code_at<ENC>(P.pool, S.v_pos, S.vdir, S.n, int64_t(fd) - S.ubase);
@@ -326,7 +326,6 @@ __device__ __forceinline__ int xstep(TState<K, MODE>& S, int32_t (&cur)[K], int3
             for (int w = 0; w < St::NW - 1; ++w) S.HW[w] = __funnelshift_r(S.HW[w], S.HW[w + 1], 2);
             S.HW[St::NW - 1] = __funnelshift_r(S.HW[St::NW - 1], S.rh.cur, 2);
             S.rh.cur >>= 2;
-            if (--S.rh.cnt == 0) S.rh.refill(P.pool);
         } else {
             constexpr int ENC = MODE == 1 ? ENC_2BIT : ENC_5BIT;
             const uint32_t code =
@@ -410,6 +409,7 @@ __global__ void __launch_bounds__(kTB, tier_min_blocks<K>()) thread_tier_kernel(
     int32_t E[K], O[K];
     bool active = false;
     long long qidx = 0;
+    unsigned it = 0;  // warp-uniform iteration counter (2 antidiagonals each)
     auto fetch = [&]() {
         active = false;
         uint32_t unit;
@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(kTB, tier_min_blocks<K>()) thread_tier_kernel(
                 if (P.pilot) P.pilot_w[qidx] = -2;  // not a thread-tier unit
                 continue;
             }
-            start_unit<K, MODE>(S, E, O, P, unit, X);
+            start_unit<K, MODE>(S, E, O, P, unit, X, it);
             active = true;
             return;
         }
@@ -428,9 +428,15 @@ __global__ void __launch_bounds__(kTB, tier_min_blocks<K>()) thread_tier_kernel(
 
     while (__any_sync(0xFFFFFFFFu, active)) {
         if (active) {
+            if constexpr (MODE == 0) {
+                if ((it & 15) == 0) {  // the same iteration for every thread
+                    S.rv.refill(P.pool);
+                    S.rh.refill(P.pool);
+                }
+            }
             int32_t spread = 0;
-            int r = xstep<K, MODE, true>(S, O, E, P, tab, gap, X, spread);
-            if (r == kGo) r = xstep<K, MODE, false>(S, E, O, P, tab, gap, X, spread);
+            int r = xstep<K, MODE, true>(S, O, E, P, tab, gap, X, spread, it);
+            if (r == kGo) r = xstep<K, MODE, false>(S, E, O, P, tab, gap, X, spread, it);
             if (r != kGo) {
                 if (P.pilot) {
                     P.pilot_w[qidx] = r == kEscalate ? -1 : S.delta_w;
@@ -460,6 +466,7 @@ __global__ void __launch_bounds__(kTB, tier_min_blocks<K>()) thread_tier_kernel(
                 fetch();
             }
         }
+        ++it;
     }
     if (P.pilot) return;
     if (my_units) atomicAdd(&P.ctr->units[P.tier], my_units);
