@@ -409,7 +409,9 @@ __global__ void __launch_bounds__(kTB, tier_min_blocks<K>()) thread_tier_kernel(
     int32_t E[K], O[K];
     bool active = false;
     long long qidx = 0;
-    unsigned it = 0;  // warp-uniform iteration counter (2 antidiagonals each)
+    // warp-uniform iteration counter (2 antidiagonals each); the first units
+    // start "at the end of iteration -1"
+    unsigned it = 0xFFFFFFFFu;
     auto fetch = [&]() {
         active = false;
         uint32_t unit;
@@ -425,6 +427,7 @@ __global__ void __launch_bounds__(kTB, tier_min_blocks<K>()) thread_tier_kernel(
         }
     };
     fetch();
+    it = 0;
 
     while (__any_sync(0xFFFFFFFFu, active)) {
         if (active) {
