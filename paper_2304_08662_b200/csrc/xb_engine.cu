@@ -1107,7 +1107,7 @@ int xb_measure_int32_peak(int device, double* alu, double* mixed, double* clk_mh
             std::vector<long long> c(static_cast<size_t>(blocks));
             CK(cudaMemcpy(c.data(), clk, size_t(blocks) * 8, cudaMemcpyDeviceToHost));
             const long long cmax = *std::max_element(c.begin(), c.end());
-            const double ops = double(blocks) * tb * iters * (v == 0 ? 24.0 : 32.0);
+            const double ops = double(blocks) * tb * iters * 32.0;  // 32 SASS instructions per iteration
             // per-SM clock cycles: blocks run concurrently (bps resident per SM)
             const double per_clk_sm = ops / (double(cmax) * sms);
             res[v] = std::max(res[v], per_clk_sm);

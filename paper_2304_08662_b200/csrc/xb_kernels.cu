@@ -248,21 +248,23 @@ __global__ void prep_kernel(PrepParams P) {
 }
 
 // ------------------------------------------------ INT32 microbenchmark ----
-// Independent dependency chains, 8 per thread, unrolled; each iteration of
-// the alu variant is 8 x (VIADDMNMX, IMNMX, IADD3) = 24 ALU lane-ops.
+// Independent dependency chains, 8 per thread, each step one SASS instruction
+// that ptxas cannot fuse or move to another pipe:
+//   alu:   VIADDMNMX (the integer ALU pipe: IADD3/IMNMX/VIADDMNMX class)
+//   mixed: VIADDMNMX + IMAD (ALU pipe + FMA pipe: the SM's INT32 issue ceiling)
+// Verified in SASS (build/xb_kernels.o): the loop bodies hold exactly these.
 
 __global__ void int_peak_alu(int32_t* out, int iters, int32_t seed, long long* clk) {
-    int32_t a[8], b = seed ^ threadIdx.x, c = seed + 7;
+    int32_t a[8];
+    const int32_t b = seed ^ int32_t(threadIdx.x), c = seed + 7;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) a[q] = threadIdx.x * (q + 3);
+    for (int q = 0; q < 8; ++q) a[q] = int32_t(threadIdx.x) * (q + 3);
     long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            a[q] = __viaddmax_s32(a[q], b, c);
-            a[q] = max(a[q], b - q);
-            asm volatile("add.s32 %0, %0, %1;" : "+r"(a[q]) : "r"(c));
-        }
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int q = 0; q < 8; ++q) a[q] = __viaddmax_s32(a[q], b, c);
     }
     long long t1 = clock64();
     int32_t s = 0;
@@ -272,21 +274,20 @@ __global__ void int_peak_alu(int32_t* out, int iters, int32_t seed, long long* c
     if (threadIdx.x == 0) clk[blockIdx.x] = t1 - t0;
 }
 
-// the thread tier's own mix: per slot 6 ALU (LOP3, VIMNMX3, VIADDMNMX, ISETP,
-// SEL, SHF) + LEA/LEA.HI, measured as achieved lane-ops/clk
 __global__ void int_peak_mixed(int32_t* out, int iters, int32_t seed, long long* clk) {
-    int32_t a[8], b = seed ^ threadIdx.x, c = seed + 7;
+    int32_t a[8];
+    const int32_t b = seed ^ int32_t(threadIdx.x), c = seed + 7;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) a[q] = threadIdx.x * (q + 3);
+    for (int q = 0; q < 8; ++q) a[q] = int32_t(threadIdx.x) * (q + 3);
     long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            a[q] = __viaddmax_s32(a[q], b, c);
-            asm volatile("mad.lo.s32 %0, %0, %1, %2;" : "+r"(a[q]) : "r"(b), "r"(c));
-            a[q] = max(a[q], b - q);
-            asm volatile("mad.lo.s32 %0, %0, %1, %2;" : "+r"(a[q]) : "r"(c), "r"(b));
-        }
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                a[q] = __viaddmax_s32(a[q], b, c);
+                asm volatile("mad.lo.s32 %0, %0, %1, %2;" : "+r"(a[q]) : "r"(b), "r"(c));
+            }
     }
     long long t1 = clock64();
     int32_t s = 0;

@@ -265,3 +265,16 @@ def test_pipeline_drop_in(xb):
         for f in failed:
             got.append(f"# failed\ttask {f.task_id} side {f.side} spread {f.observed_spread}")
         assert got == p["rows"], name
+
+
+def test_multi_device_sharding_same_results(xb):
+    """xb_exec with several device ids shards tasks LPT across them (here two
+    shards on one GPU: no collective, host gather by task index)."""
+    from paper_2304_08662_b200 import synth
+    ds = synth.make(5, 0.001)
+    pool = _config_pool(xb, ds)
+    a, sa = xb.extend_tasks(pool, ds.tasks, ds.k, ds.band)
+    b, sb = xb.extend_tasks(pool, ds.tasks, ds.k, ds.band, n_devices=2, device_ids=[0, 0])
+    assert result_rows_equal(a, b).all() and (sa == sb).all()
+    st = xb.xband.last_stats()
+    assert st["n_devices"] == 2
