@@ -240,6 +240,8 @@ struct DevPool {
     bool ready = false;
 };
 
+struct Workspace;
+
 struct xb_pool {
     xb_scheme scheme;
     std::vector<char> symbols;
@@ -253,6 +255,7 @@ struct xb_pool {
     std::vector<int64_t> seq_pos, seq_len;
     DevScheme dev_scheme{};
     std::map<int, DevPool> dev;
+    std::map<int, std::vector<Workspace*>> ws;  // reusable per-device batch buffers
     std::mutex mu;
 };
 
@@ -383,6 +386,8 @@ static void pool_drop_devices(xb_pool* p) {
     p->dev.clear();
 }
 
+static void destroy_workspaces(xb_pool* p);
+
 extern "C" {
 
 xb_pool* xb_pool_create(const xb_scheme* s, int* err) {
@@ -451,6 +456,7 @@ void xb_pool_evict(xb_pool* p) {
 
 void xb_pool_free(xb_pool* p) {
     if (!p) return;
+    destroy_workspaces(p);
     pool_drop_devices(p);
     if (p->host_words) cudaFreeHost(p->host_words);
     delete p;
@@ -460,10 +466,87 @@ void xb_pool_free(xb_pool* p) {
 
 // ------------------------------------------------------------------ batch ----
 
+// Device buffers + pinned staging of one batch on one device.  Cached per
+// (pool, device) and reused by later batches, so repeated calls do not pay
+// cudaMalloc / page-locking on every step.
+struct Workspace {
+    int dev = 0;
+    bool in_use = false;
+    int64_t capU = 0, capI = 0;
+    size_t scratch_bytes = 0, cub_bytes = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev[12] = {};
+    int64_t* d_tasks = nullptr;
+    DevUnit* d_units = nullptr;
+    uint32_t *d_keys = nullptr, *d_vals = nullptr, *d_keys2 = nullptr, *d_order = nullptr;
+    DevResult* d_res = nullptr;
+    int32_t* d_seed = nullptr;
+    uint32_t* d_lists = nullptr;
+    DevCounters* d_ctr = nullptr;
+    int32_t* d_scratch = nullptr;
+    int32_t* d_pilot = nullptr;
+    void* d_cub = nullptr;
+    DevResult* h_res = nullptr;
+    int32_t* h_seed = nullptr;
+    int64_t* h_tasks = nullptr;
+
+    void release_units() {
+        cudaFree(d_units);
+        cudaFree(d_keys);
+        cudaFree(d_vals);
+        cudaFree(d_keys2);
+        cudaFree(d_order);
+        cudaFree(d_res);
+        cudaFree(d_lists);
+        cudaFree(d_pilot);
+        cudaFree(d_cub);
+        if (h_res) cudaFreeHost(h_res);
+        d_units = nullptr;
+        d_keys = d_vals = d_keys2 = d_order = d_lists = nullptr;
+        d_res = nullptr;
+        d_pilot = nullptr;
+        d_cub = nullptr;
+        h_res = nullptr;
+        capU = 0;
+        cub_bytes = 0;
+    }
+    void release_items() {
+        cudaFree(d_tasks);
+        cudaFree(d_seed);
+        if (h_seed) cudaFreeHost(h_seed);
+        if (h_tasks) cudaFreeHost(h_tasks);
+        d_tasks = nullptr;
+        d_seed = nullptr;
+        h_seed = nullptr;
+        h_tasks = nullptr;
+        capI = 0;
+    }
+    void destroy() {
+        cudaSetDevice(dev);
+        release_units();
+        release_items();
+        cudaFree(d_ctr);
+        cudaFree(d_scratch);
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+static void destroy_workspaces(xb_pool* p) {
+    for (auto& kv : p->ws)
+        for (Workspace* w : kv.second) {
+            w->destroy();
+            delete w;
+        }
+    p->ws.clear();
+}
+
 struct DevBatch {
     int dev = 0;
     cudaStream_t stream = nullptr;
-    bool own_stream = false;
+    Workspace* ws = nullptr;
+    bool ws_cached = false;
     DevPool* pool = nullptr;
     std::vector<int64_t> tasks;  // global task (or unit) indices of this shard
     int64_t n_items = 0;         // tasks (or units) on this device
@@ -480,7 +563,7 @@ struct DevBatch {
     int scratch_warps = 0;
     void* d_cub = nullptr;
     size_t cub_bytes = 0;
-    cudaEvent_t ev[12] = {};
+    cudaEvent_t* ev = nullptr;
     int sm_count = 0;
     int occ[5] = {0, 0, 0, 0, 0};
     int mode = 0;
@@ -488,6 +571,7 @@ struct DevBatch {
     // host staging (pinned)
     DevResult* h_res = nullptr;
     int32_t* h_seed = nullptr;
+    int64_t* h_tasks = nullptr;
     // host-built units (units mode)
     std::vector<DevUnit> h_units;
 };
@@ -502,26 +586,16 @@ struct xb_batch {
     bool ran = false;
 };
 
-static void free_dev(DevBatch& D) {
-    cudaSetDevice(D.dev);
-    cudaFree(D.d_tasks);
-    cudaFree(D.d_units);
-    cudaFree(D.d_keys);
-    cudaFree(D.d_vals);
-    cudaFree(D.d_keys2);
-    cudaFree(D.d_order);
-    cudaFree(D.d_res);
-    cudaFree(D.d_seed);
-    cudaFree(D.d_lists);
-    cudaFree(D.d_ctr);
-    cudaFree(D.d_scratch);
-    cudaFree(D.d_pilot);
-    cudaFree(D.d_cub);
-    for (auto& e : D.ev)
-        if (e) cudaEventDestroy(e);
-    if (D.own_stream && D.stream) cudaStreamDestroy(D.stream);
-    if (D.h_res) cudaFreeHost(D.h_res);
-    if (D.h_seed) cudaFreeHost(D.h_seed);
+static void free_dev(xb_pool* p, DevBatch& D) {
+    if (!D.ws) return;
+    if (D.ws_cached) {
+        std::lock_guard<std::mutex> g(p->mu);
+        D.ws->in_use = false;
+    } else {
+        D.ws->destroy();
+        delete D.ws;
+    }
+    D.ws = nullptr;
 }
 
 // longest-first estimate for a unit, shared with the prep kernel
@@ -531,38 +605,67 @@ static inline long long unit_est(long long hl, long long vl) {
     return 2 * mn + std::min(gd, 64LL);
 }
 
+static Workspace* acquire_workspace(xb_pool* p, int dev, bool* cached) {
+    std::lock_guard<std::mutex> g(p->mu);
+    auto& v = p->ws[dev];
+    for (Workspace* w : v)
+        if (!w->in_use) {
+            w->in_use = true;
+            *cached = true;
+            return w;
+        }
+    auto* w = new Workspace();
+    w->dev = dev;
+    w->in_use = true;
+    if (v.size() < 2) {  // keep a couple per device; extra concurrent batches are transient
+        v.push_back(w);
+        *cached = true;
+    } else {
+        *cached = false;
+    }
+    return w;
+}
+
 static int setup_device(xb_batch* B, DevBatch& D, const xb_exec* ex) {
     CK(cudaSetDevice(D.dev));
-    if (ex && ex->stream && B->devs.size() == 1) {
-        D.stream = (cudaStream_t)ex->stream;
-    } else {
-        CK(cudaStreamCreateWithFlags(&D.stream, cudaStreamNonBlocking));
-        D.own_stream = true;
+    D.ws = acquire_workspace(B->pool, D.dev, &D.ws_cached);
+    Workspace& W = *D.ws;
+    if (!W.stream) {
+        CK(cudaStreamCreateWithFlags(&W.stream, cudaStreamNonBlocking));
+        for (auto& e : W.ev) CK(cudaEventCreate(&e));
+        CK(cudaMalloc(&W.d_ctr, sizeof(DevCounters)));
     }
-    for (auto& e : D.ev) CK(cudaEventCreate(&e));
+    D.stream = (ex && ex->stream && B->devs.size() == 1) ? (cudaStream_t)ex->stream : W.stream;
+    D.ev = W.ev;
     CK(cudaDeviceGetAttribute(&D.sm_count, cudaDevAttrMultiProcessorCount, D.dev));
     const int rc = pool_device(B->pool, D.dev, D.stream, &B->h2d, &D.pool);
     if (rc) return rc;
-    const int64_t nu = D.n_units;
-    const size_t U = size_t(std::max<int64_t>(nu, 1));
-    CK(cudaMalloc(&D.d_units, U * sizeof(DevUnit)));
-    CK(cudaMalloc(&D.d_keys, U * 4));
-    CK(cudaMalloc(&D.d_vals, U * 4));
-    CK(cudaMalloc(&D.d_keys2, U * 4));
-    CK(cudaMalloc(&D.d_order, U * 4));
-    CK(cudaMalloc(&D.d_res, U * sizeof(DevResult)));
-    CK(cudaMalloc(&D.d_lists, U * 4 * kNumTiers));
-    CK(cudaMalloc(&D.d_ctr, sizeof(DevCounters)));
-    CK(cudaMalloc(&D.d_pilot, (U / 512 + 128) * 4));
-    CK(cudaMallocHost(&D.h_res, U * sizeof(DevResult)));
-    if (!B->units_mode) {
-        CK(cudaMalloc(&D.d_tasks, size_t(std::max<int64_t>(D.n_items, 1)) * 32));
-        CK(cudaMalloc(&D.d_seed, size_t(std::max<int64_t>(D.n_items, 1)) * 4));
-        CK(cudaMallocHost(&D.h_seed, size_t(std::max<int64_t>(D.n_items, 1)) * 4));
+    const int64_t U = std::max<int64_t>(D.n_units, 1);
+    if (U > W.capU) {
+        W.release_units();
+        CK(cudaMalloc(&W.d_units, size_t(U) * sizeof(DevUnit)));
+        CK(cudaMalloc(&W.d_keys, size_t(U) * 4));
+        CK(cudaMalloc(&W.d_vals, size_t(U) * 4));
+        CK(cudaMalloc(&W.d_keys2, size_t(U) * 4));
+        CK(cudaMalloc(&W.d_order, size_t(U) * 4));
+        CK(cudaMalloc(&W.d_res, size_t(U) * sizeof(DevResult)));
+        CK(cudaMalloc(&W.d_lists, size_t(U) * 4 * kNumTiers));
+        CK(cudaMalloc(&W.d_pilot, size_t(U / 512 + 128) * 4));
+        CK(cudaMallocHost(&W.h_res, size_t(U) * sizeof(DevResult)));
+        CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, W.cub_bytes, W.d_keys, W.d_keys2,
+                                                     W.d_vals, W.d_order, int(U), 0, 32, D.stream));
+        CK(cudaMalloc(&W.d_cub, std::max<size_t>(W.cub_bytes, 16)));
+        W.capU = U;
     }
-    CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, D.cub_bytes, D.d_keys, D.d_keys2,
-                                                 D.d_vals, D.d_order, int(U), 0, 32, D.stream));
-    CK(cudaMalloc(&D.d_cub, std::max<size_t>(D.cub_bytes, 16)));
+    const int64_t I = std::max<int64_t>(D.n_items, 1);
+    if (!B->units_mode && I > W.capI) {
+        W.release_items();
+        CK(cudaMalloc(&W.d_tasks, size_t(I) * 32));
+        CK(cudaMalloc(&W.d_seed, size_t(I) * 4));
+        CK(cudaMallocHost(&W.h_seed, size_t(I) * 4));
+        CK(cudaMallocHost(&W.h_tasks, size_t(I) * 32));
+        W.capI = I;
+    }
     // warp-tier scratch: 2*band ints per resident warp, capped at 1 GiB
     {
         const int64_t per_warp = 2LL * B->band * 4;
@@ -570,8 +673,30 @@ static int setup_device(xb_batch* B, DevBatch& D, const xb_exec* ex) {
         warps = std::min<int64_t>(warps, std::max<int64_t>(4, (1LL << 30) / per_warp));
         warps = (warps + 3) / 4 * 4;
         D.scratch_warps = int(warps);
-        CK(cudaMalloc(&D.d_scratch, size_t(warps * per_warp)));
+        const size_t need = size_t(warps * per_warp);
+        if (need > W.scratch_bytes) {
+            cudaFree(W.d_scratch);
+            CK(cudaMalloc(&W.d_scratch, need));
+            W.scratch_bytes = need;
+        }
     }
+    D.d_units = W.d_units;
+    D.d_keys = W.d_keys;
+    D.d_vals = W.d_vals;
+    D.d_keys2 = W.d_keys2;
+    D.d_order = W.d_order;
+    D.d_res = W.d_res;
+    D.d_lists = W.d_lists;
+    D.d_ctr = W.d_ctr;
+    D.d_pilot = W.d_pilot;
+    D.d_cub = W.d_cub;
+    D.cub_bytes = W.cub_bytes;
+    D.d_scratch = W.d_scratch;
+    D.h_res = W.h_res;
+    D.d_tasks = W.d_tasks;
+    D.d_seed = W.d_seed;
+    D.h_seed = W.h_seed;
+    D.h_tasks = W.h_tasks;
     return XB_OK;
 }
 
@@ -582,24 +707,24 @@ static int upload_inputs(xb_batch* B, DevBatch& D, const void* items) {
         if (U) {
             CK(cudaMemcpyAsync(D.d_units, D.h_units.data(), U * sizeof(DevUnit),
                                cudaMemcpyHostToDevice, D.stream));
+            CK(cudaStreamSynchronize(D.stream));  // h_units is pageable
             B->h2d += int64_t(U * sizeof(DevUnit));
         }
     } else if (D.n_items) {
         const xb_task* T = static_cast<const xb_task*>(items);
-        int64_t* h = nullptr;
-        CK(cudaMallocHost(&h, size_t(D.n_items) * 32));
-        for (int64_t q = 0; q < D.n_items; ++q) {
-            const xb_task& t = T[D.tasks.empty() ? q : D.tasks[size_t(q)]];
-            h[4 * q + 0] = t.h_id;
-            h[4 * q + 1] = t.v_id;
-            h[4 * q + 2] = int64_t(t.h_seed);
-            h[4 * q + 3] = int64_t(t.v_seed);
-        }
-        const cudaError_t e = cudaMemcpyAsync(D.d_tasks, h, size_t(D.n_items) * 32,
-                                              cudaMemcpyHostToDevice, D.stream);
-        cudaStreamSynchronize(D.stream);
-        cudaFreeHost(h);
-        CK(e);
+        int64_t* h = D.h_tasks;
+        const bool sh = !D.tasks.empty();
+        const int64_t* map = sh ? D.tasks.data() : nullptr;
+        parallel_for(D.n_items, [&](int64_t a, int64_t b) {
+            for (int64_t q = a; q < b; ++q) {
+                const xb_task& t = T[sh ? map[q] : q];
+                h[4 * q + 0] = t.h_id;
+                h[4 * q + 1] = t.v_id;
+                h[4 * q + 2] = int64_t(t.h_seed);
+                h[4 * q + 3] = int64_t(t.v_seed);
+            }
+        });
+        CK(cudaMemcpyAsync(D.d_tasks, h, size_t(D.n_items) * 32, cudaMemcpyHostToDevice, D.stream));
         B->h2d += D.n_items * 32;
     }
     return XB_OK;
@@ -927,7 +1052,10 @@ int xb_batch_fetch(xb_batch* B, xb_side_result* out, int32_t* seed_score) {
                 std::memcpy(&out[g], &D.h_res[q], sizeof(xb_side_result));
             }
         } else if (!sharded) {
-            std::memcpy(out, D.h_res, size_t(D.n_units) * sizeof(xb_side_result));
+            const DevResult* src = D.h_res;
+            parallel_for(D.n_units, [&](int64_t a, int64_t b) {
+                std::memcpy(out + a, src + a, size_t(b - a) * sizeof(xb_side_result));
+            });
             if (seed_score) std::memcpy(seed_score, D.h_seed, size_t(D.n_items) * 4);
         } else {
             for (int64_t q = 0; q < D.n_items; ++q) {
@@ -978,7 +1106,7 @@ int xb_batch_stats(xb_batch* B, xb_stats* st) {
 
 void xb_batch_free(xb_batch* B) {
     if (!B) return;
-    for (auto& D : B->devs) free_dev(D);
+    for (auto& D : B->devs) free_dev(B->pool, D);
     delete B;
 }
 

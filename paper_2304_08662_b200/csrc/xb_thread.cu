@@ -70,6 +70,16 @@ __device__ __forceinline__ void init_windows(TState<K, MODE>& S, const uint32_t*
     }
 }
 
+// First antidiagonal at which the band's slot range reaches past the matrix
+// (i > n for slot 0, j > m for slot K-1) and the step must mask slots, and the
+// first at which anything else forces the rare path (end of the matrix,
+// pilot cap).
+template <int K, int MODE>
+__device__ __forceinline__ void set_limits(TState<K, MODE>& S) {
+    S.d_vm = min(2 * (S.ubase + S.n + 1), 2 * (S.m - S.ubase - K + 2) - 1);
+    S.d_lim = min(S.d_vm, min(S.n + S.m + 2, S.dcap + 1));
+}
+
 template <int K, int MODE>
 __device__ __forceinline__ void start_unit(TState<K, MODE>& S, int32_t (&E)[K], int32_t (&O)[K],
                                            const TierParams& P, uint32_t unit, int32_t X, unsigned it) {
@@ -84,10 +94,10 @@ __device__ __forceinline__ void start_unit(TState<K, MODE>& S, int32_t (&E)[K], 
     S.d = 1;
     S.dcap = P.pilot ? P.pilot_cap : INT_MAX;
     S.ubase = -(K / 2);
-    S.fl1 = 0;  // antidiagonal 0: the origin
-    S.ll1 = 0;
-    S.fl2 = kBig;  // antidiagonal -1: empty
-    S.ll2 = -kBig;
+    S.ls1 = S.hs1 = K / 2;  // antidiagonal 0: the origin, u = 0
+    S.ls2 = kBig;           // antidiagonal -1: empty
+    S.hs2 = -kBig;
+    set_limits(S);
     S.T = 0;
     S.best_d = 0;
     S.best_i = 0;
@@ -192,71 +202,77 @@ __device__ __forceinline__ int xstep(TState<K, MODE>& S, int32_t (&cur)[K], int3
                                      int32_t gap, int32_t X, int32_t& spread, unsigned it) {
     using St = TState<K, MODE>;
     const int d = S.d;
-    // reachable window (align.cpp:68-81); an empty row is [kBig, -kBig] so
-    // the min/max need no liveness tests
-    const int lo_u = min(S.fl1, S.fl2 + 1);
-    const int hi_u = max(S.ll1, S.ll2) + 1;
-    const int lo = __vimax3_s32(lo_u, d - S.m, 0);
-    const int hi = __vimin3_s32(hi_u, d, S.n);
-    const int w = hi - lo + 1;  // <= 0: empty window, counts nothing (align.cpp:84-91)
-    const int fd = d >> 1, cd = d - fd;
-    const int s_lo = fd - hi_u - S.ubase, s_hi = fd - lo_u - S.ubase;
-    // one rarely-taken branch for every way a step can stop or reshape
-    if (lo_u >= kBig || d > S.dcap || w > P.band || s_lo < 0 || s_hi > K - 1) {
-        if (lo_u >= kBig || d > S.n + S.m + 1) return kDone;  // align.cpp:64-66
+    // Reachable window (align.cpp:68-81) in slot space: a gap step from row
+    // d-1 reaches slots [ls1-1, hs1] (d odd) or [ls1, hs1+1] (d even), a
+    // diagonal step from d-2 the same slots.  Empty rows are [kBig, -kBig].
+    int s_lo = ODD ? min(S.ls1 - 1, S.ls2) : min(S.ls1, S.ls2);
+    int s_hi = ODD ? max(S.hs1, S.hs2) : max(S.hs1 + 1, S.hs2);
+    const int fd = d >> 1;
+    int A = fd - S.ubase;  // slot k holds i = A - k
+    // clamp to the matrix: i <= min(d, n)  and  i >= max(d - m, 0)
+    int w = min(s_hi, A - max(d - S.m, 0)) - max(s_lo, A - min(d, S.n)) + 1;
+    uint32_t vm[St::NM];
+#pragma unroll
+    for (int q = 0; q < St::NM; ++q) vm[q] = range_bits(0, min(K - 1 - 32 * q, 31));
+    [[maybe_unused]] uint32_t vms[St::NW];
+    [[maybe_unused]] bool masked = false;
+    // one rarely-taken branch for every way a step can stop, reshape or mask
+    if (s_lo < 0 || unsigned(s_hi) > unsigned(K - 1) || w > P.band || d >= S.d_lim) {
+        if (s_hi < 0 || d > S.n + S.m + 1 || d > S.dcap) return kDone;  // align.cpp:64-66
         if (w > P.band) {  // align.cpp:93-94: first overflow, cells so far
             spread = w;
             return kBand;
         }
-        if (d > S.dcap) return kDone;  // pilot: prefix only
-        // every live source lies inside the unclamped window, so it must fit
-        const int wu = hi_u - lo_u + 1;
-        if (wu > K) return kEscalate;
-        const int nb = fd - hi_u - ((K - wu) >> 1);
-        shift_slots<K>(cur, nb - S.ubase);
-        shift_slots<K>(prv, nb - S.ubase);
-        S.ubase = nb;
-        // symbols left to consume before the next refill (iteration multiple of 16):
-        // this iteration's own consumption counts unless it already happened
-        const int to_refill = 16 - int(it & 15);
-        init_windows(S, P.pool, ODD ? to_refill : to_refill - 1, to_refill);
+        if (s_lo < 0 || s_hi > K - 1) {
+            // every live source lies inside the unclamped window, so it must fit
+            const int wu = s_hi - s_lo + 1;
+            if (wu > K) return kEscalate;
+            const int sh = s_lo - ((K - wu) >> 1);  // new slot 0 = old slot sh
+            shift_slots<K>(cur, sh);
+            shift_slots<K>(prv, sh);
+            S.ubase += sh;
+            S.ls1 -= sh;
+            S.hs1 -= sh;
+            S.ls2 -= sh;
+            S.hs2 -= sh;
+            s_lo -= sh;
+            s_hi -= sh;
+            A -= sh;
+            set_limits(S);
+            // symbols left to consume before the next refill (iteration multiple of 16):
+            // this iteration's own consumption counts unless it already happened
+            const int to_refill = 16 - int(it & 15);
+            init_windows(S, P.pool, ODD ? to_refill : to_refill - 1, to_refill);
+        }
+        if (d >= S.d_vm) {
+            // slots inside the matrix: i <= n  <=>  k >= klo ;  j <= m  <=>  k <= khi
+            const int klo = A - S.n;
+            const int khi = S.m - (d - fd) - S.ubase;
+            const int khk = min(khi, K - 1);
+#pragma unroll
+            for (int q = 0; q < St::NM; ++q) vm[q] = range_bits(max(klo - 32 * q, 0), min(khk - 32 * q, 31));
+            if constexpr (MODE == 0) {
+#pragma unroll
+                for (int ww = 0; ww < St::NW; ++ww) {
+                    const int l = max(klo - 16 * ww, 0), h = min(khi - 16 * ww, 15);
+                    vms[ww] = range_bits(2 * l, 2 * h + 1) & 0xAAAAAAAAu;
+                }
+            }
+            masked = true;
+        }
     }
     S.cells += max(w, 0);
     S.delta_w = max(S.delta_w, w);
-
-    // slots inside the matrix: i <= n  <=>  k >= klo ;  j <= m  <=>  k <= khi
-    const int klo = fd - S.ubase - S.n;
-    const int khi = S.m - cd - S.ubase;
-    uint32_t vm[St::NM];
-    [[maybe_unused]] uint32_t vms[St::NW];
-    if (klo <= 0 && khi >= K - 1) {
-#pragma unroll
-        for (int q = 0; q < St::NM; ++q) vm[q] = range_bits(0, min(K - 1 - 32 * q, 31));
-        if constexpr (MODE == 0) {
-#pragma unroll
-            for (int w = 0; w < St::NW; ++w) vms[w] = 0xAAAAAAAAu;
-        }
-    } else {
-        const int khk = min(khi, K - 1);
-#pragma unroll
-        for (int q = 0; q < St::NM; ++q) vm[q] = range_bits(max(klo - 32 * q, 0), min(khk - 32 * q, 31));
-        if constexpr (MODE == 0) {
-#pragma unroll
-            for (int w = 0; w < St::NW; ++w) {
-                const int l = max(klo - 16 * w, 0), h = min(khi - 16 * w, 15);
-                vms[w] = range_bits(2 * l, 2 * h + 1) & 0xAAAAAAAAu;
-            }
-        }
-    }
 
     // DNA +1/-1/-1: Z[w] bit 2f+1 = slot 16w+f is a match inside the matrix,
     // bit 2f = 1 (PAT), so one LOP3 per slot isolates [match][1]
     uint32_t Z[St::NW];
     if constexpr (MODE == 0) {
 #pragma unroll
-        for (int w = 0; w < St::NW; ++w) {
-            const uint32_t x = S.VW[w] ^ S.HW[w];
-            Z[w] = (~(x | (x << 1)) & vms[w]) | P.pat;
+        for (int ww = 0; ww < St::NW; ++ww) {
+            const uint32_t x = S.VW[ww] ^ S.HW[ww];
+            // common case, one LOP3: PAT | ~(x | x << 1)
+            Z[ww] = masked ? ((~(x | (x << 1)) & vms[ww]) | P.pat) : (P.pat | ~(x | (x << 1)));
         }
     }
 
@@ -281,10 +297,10 @@ __device__ __forceinline__ int xstep(TState<K, MODE>& S, int32_t (&cur)[K], int3
         if (qnew > qold) {
             S.T = qnew - beta * d - X - 1;
             S.best_d = d;
-            S.best_i = fd - S.ubase - (cf & 63);
+            S.best_i = A - (cf & 63);
         }
     }
-    // live range of row d (align.cpp:138-145); out-of-matrix slots masked
+    // live slots of row d (align.cpp:138-145); out-of-matrix slots masked
     {
         int hs, ls;
         bool any;
@@ -299,11 +315,10 @@ __device__ __forceinline__ int xstep(TState<K, MODE>& S, int32_t (&cur)[K], int3
             hs = lv1 ? 63 - __clz(lv1) : 31 - __clz(lv0);
             ls = lv0 ? __ffs(lv0) - 1 : 31 + __ffs(lv1);
         }
-        S.fl2 = S.fl1;
-        S.ll2 = S.ll1;
-        const int base = fd - S.ubase;
-        S.fl1 = any ? base - hs : kBig;
-        S.ll1 = any ? base - ls : -kBig;
+        S.ls2 = S.ls1;
+        S.hs2 = S.hs1;
+        S.ls1 = any ? ls : kBig;
+        S.hs1 = any ? hs : -kBig;
     }
 
     // feed the symbol that enters the band on d+1
@@ -329,7 +344,7 @@ __device__ __forceinline__ int xstep(TState<K, MODE>& S, int32_t (&cur)[K], int3
         } else {
             constexpr int ENC = MODE == 1 ? ENC_2BIT : ENC_5BIT;
             const uint32_t code =
-                code_at<ENC>(P.pool, S.h_pos, S.hdir, S.m, int64_t(cd) + S.ubase - 1 + St::WK);
+                code_at<ENC>(P.pool, S.h_pos, S.hdir, S.m, int64_t(d - fd) + S.ubase - 1 + St::WK);
 #pragma unroll
             for (int r = 0; r < St::NB - 1; ++r) S.HW[r] = __funnelshift_r(S.HW[r], S.HW[r + 1], 8);
             S.HW[St::NB - 1] = __funnelshift_r(S.HW[St::NB - 1], code, 8);
