@@ -163,6 +163,8 @@ struct TState {
     int32_t d, ubase, dcap;
     int32_t ls1, hs1, ls2, hs2;  // lowest/highest live slot of rows d-1, d-2; empty = (kBig, -kBig)
     int32_t d_vm, d_lim;         // first d needing matrix masks / any rare-path work
+    int32_t stop;                // 0 running, else kDone / kBand / kEscalate
+    int32_t spread;              // observed spread when stop == kBand
     int32_t T, best_d, best_i, delta_w;
     int32_t cells;               // <= 64 (n + m + 1): int32 under the prep guard
     // windows

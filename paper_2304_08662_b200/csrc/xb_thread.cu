@@ -97,6 +97,8 @@ __device__ __forceinline__ void start_unit(TState<K, MODE>& S, int32_t (&E)[K], 
     S.ls1 = S.hs1 = K / 2;  // antidiagonal 0: the origin, u = 0
     S.ls2 = kBig;           // antidiagonal -1: empty
     S.hs2 = -kBig;
+    S.stop = 0;
+    S.spread = 0;
     set_limits(S);
     S.T = 0;
     S.best_d = 0;
@@ -161,7 +163,8 @@ __device__ __forceinline__ void slot(int32_t (&cur)[K], const int32_t (&prv)[K],
     if constexpr (MODE == 0) {
         constexpr int w = k >> 4, f = k & 15;
         // t = [match bit at 2f+1][1 at 2f]  ->  (t >> 2f) = 1 + 2*match = sim - 2*gap
-        const uint32_t t = (3u << (2 * f)) & Z[w];
+        // (one LOP3: imm & (Z | PAT))
+        const uint32_t t = (3u << (2 * f)) & (Z[w] | P.pat);
         if constexpr (f == 0)
             db = dg + int32_t(t);
         else
@@ -196,10 +199,13 @@ __device__ __forceinline__ void all_slots(std::integer_sequence<int, ks...>, int
 }
 
 // One antidiagonal d.  cur holds d-2 on entry and d on exit, prv holds d-1.
+// A step that finds the unit finished (or failing, or outgrowing K) sets
+// S.stop and keeps going: the rest of the step is harmless dead work, which
+// keeps a single exit test per loop iteration instead of per-path copies.
 template <int K, int MODE, bool ODD>
-__device__ __forceinline__ int xstep(TState<K, MODE>& S, int32_t (&cur)[K], int32_t (&prv)[K],
-                                     const TierParams& P, const int8_t* __restrict__ tab,
-                                     int32_t gap, int32_t X, int32_t& spread, unsigned it) {
+__device__ __forceinline__ void xstep(TState<K, MODE>& S, int32_t (&cur)[K], int32_t (&prv)[K],
+                                      const TierParams& P, const int8_t* __restrict__ tab,
+                                      int32_t gap, int32_t X, unsigned it) {
     using St = TState<K, MODE>;
     const int d = S.d;
     // Reachable window (align.cpp:68-81) in slot space: a gap step from row
@@ -215,64 +221,67 @@ __device__ __forceinline__ int xstep(TState<K, MODE>& S, int32_t (&cur)[K], int3
 #pragma unroll
     for (int q = 0; q < St::NM; ++q) vm[q] = range_bits(0, min(K - 1 - 32 * q, 31));
     [[maybe_unused]] uint32_t vms[St::NW];
-    [[maybe_unused]] bool masked = false;
-    // one rarely-taken branch for every way a step can stop, reshape or mask
-    if (s_lo < 0 || unsigned(s_hi) > unsigned(K - 1) || w > P.band || d >= S.d_lim) {
-        if (s_hi < 0 || d > S.n + S.m + 1 || d > S.dcap) return kDone;  // align.cpp:64-66
-        if (w > P.band) {  // align.cpp:93-94: first overflow, cells so far
-            spread = w;
-            return kBand;
-        }
-        if (s_lo < 0 || s_hi > K - 1) {
-            // every live source lies inside the unclamped window, so it must fit
-            const int wu = s_hi - s_lo + 1;
-            if (wu > K) return kEscalate;
-            const int sh = s_lo - ((K - wu) >> 1);  // new slot 0 = old slot sh
-            shift_slots<K>(cur, sh);
-            shift_slots<K>(prv, sh);
-            S.ubase += sh;
-            S.ls1 -= sh;
-            S.hs1 -= sh;
-            S.ls2 -= sh;
-            S.hs2 -= sh;
-            s_lo -= sh;
-            s_hi -= sh;
-            A -= sh;
-            set_limits(S);
-            // symbols left to consume before the next refill (iteration multiple of 16):
-            // this iteration's own consumption counts unless it already happened
-            const int to_refill = 16 - int(it & 15);
-            init_windows(S, P.pool, ODD ? to_refill : to_refill - 1, to_refill);
-        }
-        if (d >= S.d_vm) {
-            // slots inside the matrix: i <= n  <=>  k >= klo ;  j <= m  <=>  k <= khi
-            const int klo = A - S.n;
-            const int khi = S.m - (d - fd) - S.ubase;
-            const int khk = min(khi, K - 1);
 #pragma unroll
-            for (int q = 0; q < St::NM; ++q) vm[q] = range_bits(max(klo - 32 * q, 0), min(khk - 32 * q, 31));
-            if constexpr (MODE == 0) {
+    for (int ww = 0; ww < St::NW; ++ww) vms[ww] = 0xAAAAAAAAu;
+    // one rarely-taken branch for every way a step can stop, reshape or mask
+    if ((s_lo < 0 || unsigned(s_hi) > unsigned(K - 1) || w > P.band || d >= S.d_lim) && !S.stop) {
+        if (s_hi < 0 || d > S.n + S.m + 1 || d > S.dcap) {
+            S.stop = kDone;  // align.cpp:64-66
+        } else if (w > P.band) {  // align.cpp:93-94: first overflow, cells so far
+            S.stop = kBand;
+            S.spread = w;
+        } else {
+            if (s_lo < 0 || s_hi > K - 1) {
+                // every live source lies inside the unclamped window, so it must fit
+                const int wu = s_hi - s_lo + 1;
+                if (wu > K) {
+                    S.stop = kEscalate;
+                } else {
+                    const int sh = s_lo - ((K - wu) >> 1);  // new slot 0 = old slot sh
+                    shift_slots<K>(cur, sh);
+                    shift_slots<K>(prv, sh);
+                    S.ubase += sh;
+                    S.ls1 -= sh;
+                    S.hs1 -= sh;
+                    S.ls2 -= sh;
+                    S.hs2 -= sh;
+                    A -= sh;
+                    set_limits(S);
+                    // symbols left to consume before the next refill (iteration multiple
+                    // of 16): this iteration's own consumption counts unless it happened
+                    const int to_refill = 16 - int(it & 15);
+                    init_windows(S, P.pool, ODD ? to_refill : to_refill - 1, to_refill);
+                }
+            }
+            if (d >= S.d_vm) {
+                // slots inside the matrix: i <= n  <=>  k >= klo ;  j <= m  <=>  k <= khi
+                const int klo = A - S.n;
+                const int khi = S.m - (d - fd) - S.ubase;
+                const int khk = min(khi, K - 1);
+#pragma unroll
+                for (int q = 0; q < St::NM; ++q)
+                    vm[q] = range_bits(max(klo - 32 * q, 0), min(khk - 32 * q, 31));
 #pragma unroll
                 for (int ww = 0; ww < St::NW; ++ww) {
                     const int l = max(klo - 16 * ww, 0), h = min(khi - 16 * ww, 15);
                     vms[ww] = range_bits(2 * l, 2 * h + 1) & 0xAAAAAAAAu;
                 }
             }
-            masked = true;
         }
     }
-    S.cells += max(w, 0);
-    S.delta_w = max(S.delta_w, w);
+    if (!S.stop) {
+        S.cells += max(w, 0);
+        S.delta_w = max(S.delta_w, w);
+    }
 
-    // DNA +1/-1/-1: Z[w] bit 2f+1 = slot 16w+f is a match inside the matrix,
-    // bit 2f = 1 (PAT), so one LOP3 per slot isolates [match][1]
+    // DNA +1/-1/-1: Z[w] bit 2f+1 = slot 16w+f is a match inside the matrix
+    // (one LOP3: ~(x | x << 1) & validity)
     uint32_t Z[St::NW];
     if constexpr (MODE == 0) {
 #pragma unroll
         for (int ww = 0; ww < St::NW; ++ww) {
             const uint32_t x = S.VW[ww] ^ S.HW[ww];
-            // common case, one LOP3: PAT | ~(x | x << 1)
-            Z[ww] = masked ? ((~(x | (x << 1)) & vms[ww]) | P.pat) : (P.pat | ~(x | (x << 1)));
+            Z[ww] = ~(x | (x << 1)) & vms[ww];
         }
     }
 
@@ -294,7 +303,7 @@ __device__ __forceinline__ int xstep(TState<K, MODE>& S, int32_t (&cur)[K], int3
         const int32_t cf = C.c + ((X << 6) + 63);
         const int32_t qnew = cf >> 6;
         const int32_t qold = S.T + beta * d + X + 1;
-        if (qnew > qold) {
+        if (qnew > qold && !S.stop) {
             S.T = qnew - beta * d - X - 1;
             S.best_d = d;
             S.best_i = A - (cf & 63);
@@ -351,7 +360,6 @@ __device__ __forceinline__ int xstep(TState<K, MODE>& S, int32_t (&cur)[K], int3
         }
     }
     S.d = d + 1;
-    return kGo;
 }
 
 // Work source of a launch.  Pilot: a strided sample of the order.  Cascade:
@@ -452,10 +460,10 @@ __global__ void __launch_bounds__(kTB, tier_min_blocks<K>()) thread_tier_kernel(
                     S.rh.refill(P.pool);
                 }
             }
-            int32_t spread = 0;
-            int r = xstep<K, MODE, true>(S, O, E, P, tab, gap, X, spread, it);
-            if (r == kGo) r = xstep<K, MODE, false>(S, E, O, P, tab, gap, X, spread, it);
-            if (r != kGo) {
+            xstep<K, MODE, true>(S, O, E, P, tab, gap, X, it);
+            xstep<K, MODE, false>(S, E, O, P, tab, gap, X, it);
+            if (S.stop) {
+                const int r = S.stop;
                 if (P.pilot) {
                     P.pilot_w[qidx] = r == kEscalate ? -1 : S.delta_w;
                 } else if (r == kEscalate) {
@@ -469,7 +477,7 @@ __global__ void __launch_bounds__(kTB, tier_min_blocks<K>()) thread_tier_kernel(
                     if (r == kBand) {
                         res.score = res.h_ext = res.v_ext = 0;
                         res.status = kStatusBand;
-                        res.spread = spread;
+                        res.spread = S.spread;
                     } else {
                         res.score = S.T;
                         res.h_ext = S.best_d - S.best_i;
