@@ -98,6 +98,7 @@ typedef struct {
     int64_t h2d_bytes, d2h_bytes;
     int32_t sm_count;
     int32_t start_tier;          /* tier the pilot chose */
+    int64_t dbg[6];              /* instrumented builds only (-DXB_COUNTERS=1), else 0 */
 } xb_stats;
 
 typedef struct xb_scheme xb_scheme;

@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libxdrop_b200.so")
+LIB_PATH = os.environ.get("XB_LIB_PATH") or os.path.join(HERE, "_lib", "libxdrop_b200.so")
 
 XB_OK = 0
 XB_E_BAD_PARAM = 1
@@ -62,7 +62,7 @@ class XbStats(C.Structure):
                 ("ms_prep", C.c_double), ("ms_pilot", C.c_double), ("ms_tier", C.c_double * 6),
                 ("units_tier", C.c_int64 * 6), ("cells_tier", C.c_int64 * 6),
                 ("escalated", C.c_int64 * 6), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
-                ("sm_count", C.c_int32), ("start_tier", C.c_int32)]
+                ("sm_count", C.c_int32), ("start_tier", C.c_int32), ("dbg", C.c_int64 * 6)]
 
     def as_dict(self) -> dict:
         return {"n_devices": self.n_devices, "launches": self.launches,
@@ -70,7 +70,8 @@ class XbStats(C.Structure):
                 "ms_tier": list(self.ms_tier), "units_tier": list(self.units_tier),
                 "cells_tier": list(self.cells_tier), "escalated": list(self.escalated),
                 "h2d_bytes": self.h2d_bytes, "d2h_bytes": self.d2h_bytes,
-                "sm_count": self.sm_count, "start_tier": self.start_tier}
+                "sm_count": self.sm_count, "start_tier": self.start_tier,
+                "dbg": list(self.dbg)}
 
 
 _lib = None

@@ -1096,6 +1096,7 @@ int xb_batch_stats(xb_batch* B, xb_stats* st) {
             st->escalated[t] += int64_t(c.escalated[t]);
         }
         st->start_tier = c.start_tier;
+        for (int q = 0; q < 6; ++q) st->dbg[q] += int64_t(c.dbg[q]);
         st->launches += D.launches;
         st->sm_count = D.sm_count;
     }

@@ -54,6 +54,7 @@ struct DevCounters {
     unsigned long long units[8];
     unsigned long long cells[8];
     unsigned long long escalated[8];
+    unsigned long long dbg[8];         // XB_COUNTERS builds: steps, rare, masked, recenters, stops
     int32_t start_tier;                // chosen by the pilot
     int32_t pad;
 };

@@ -15,6 +15,16 @@
 
 #include "xb_kernels.cuh"
 
+#ifndef XB_COUNTERS
+#define XB_COUNTERS 0
+#endif
+#if XB_COUNTERS
+#define XB_COUNT(i) (++xb_dbg[i])
+__device__ unsigned long long xb_dbg_unused;
+#else
+#define XB_COUNT(i) ((void)0)
+#endif
+
 namespace xb {
 
 __device__ __forceinline__ uint32_t range_bits(int lo, int hi) {
@@ -92,7 +102,7 @@ __device__ __forceinline__ void start_unit(TState<K, MODE>& S, int32_t (&E)[K], 
     S.hdir = u.dir & 1;
     S.vdir = (u.dir >> 1) & 1;
     S.d = 1;
-    S.dcap = P.pilot ? P.pilot_cap : INT_MAX;
+    S.dcap = P.pilot ? P.pilot_cap : (INT_MAX >> 1);
     S.ubase = -(K / 2);
     S.ls1 = S.hs1 = K / 2;  // antidiagonal 0: the origin, u = 0
     S.ls2 = kBig;           // antidiagonal -1: empty
@@ -205,8 +215,13 @@ __device__ __forceinline__ void all_slots(std::integer_sequence<int, ks...>, int
 template <int K, int MODE, bool ODD>
 __device__ __forceinline__ void xstep(TState<K, MODE>& S, int32_t (&cur)[K], int32_t (&prv)[K],
                                       const TierParams& P, const int8_t* __restrict__ tab,
-                                      int32_t gap, int32_t X, unsigned it) {
+                                      int32_t gap, int32_t X, unsigned it
+#if XB_COUNTERS
+                                      , unsigned long long (&xb_dbg)[8]
+#endif
+                                      ) {
     using St = TState<K, MODE>;
+    XB_COUNT(0);
     const int d = S.d;
     // Reachable window (align.cpp:68-81) in slot space: a gap step from row
     // d-1 reaches slots [ls1-1, hs1] (d odd) or [ls1, hs1+1] (d even), a
@@ -225,6 +240,7 @@ __device__ __forceinline__ void xstep(TState<K, MODE>& S, int32_t (&cur)[K], int
     for (int ww = 0; ww < St::NW; ++ww) vms[ww] = 0xAAAAAAAAu;
     // one rarely-taken branch for every way a step can stop, reshape or mask
     if ((s_lo < 0 || unsigned(s_hi) > unsigned(K - 1) || w > P.band || d >= S.d_lim) && !S.stop) {
+        XB_COUNT(1);
         if (s_hi < 0 || d > S.n + S.m + 1 || d > S.dcap) {
             S.stop = kDone;  // align.cpp:64-66
         } else if (w > P.band) {  // align.cpp:93-94: first overflow, cells so far
@@ -237,6 +253,7 @@ __device__ __forceinline__ void xstep(TState<K, MODE>& S, int32_t (&cur)[K], int
                 if (wu > K) {
                     S.stop = kEscalate;
                 } else {
+                    XB_COUNT(3);
                     const int sh = s_lo - ((K - wu) >> 1);  // new slot 0 = old slot sh
                     shift_slots<K>(cur, sh);
                     shift_slots<K>(prv, sh);
@@ -254,6 +271,7 @@ __device__ __forceinline__ void xstep(TState<K, MODE>& S, int32_t (&cur)[K], int
                 }
             }
             if (d >= S.d_vm) {
+                XB_COUNT(2);
                 // slots inside the matrix: i <= n  <=>  k >= klo ;  j <= m  <=>  k <= khi
                 const int klo = A - S.n;
                 const int khi = S.m - (d - fd) - S.ubase;
@@ -427,6 +445,9 @@ __global__ void __launch_bounds__(kTB, tier_min_blocks<K>()) thread_tier_kernel(
     uint32_t* esc_list = P.lists + (long long)next_tier * P.n_units;
     unsigned long long* esc_len = &P.ctr->list_len[next_tier];
     unsigned long long my_units = 0, my_cells = 0, my_esc = 0;
+#if XB_COUNTERS
+    unsigned long long xb_dbg[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
 
     TState<K, MODE> S;
     int32_t E[K], O[K];
@@ -460,9 +481,15 @@ __global__ void __launch_bounds__(kTB, tier_min_blocks<K>()) thread_tier_kernel(
                     S.rh.refill(P.pool);
                 }
             }
+#if XB_COUNTERS
+            xstep<K, MODE, true>(S, O, E, P, tab, gap, X, it, xb_dbg);
+            xstep<K, MODE, false>(S, E, O, P, tab, gap, X, it, xb_dbg);
+#else
             xstep<K, MODE, true>(S, O, E, P, tab, gap, X, it);
             xstep<K, MODE, false>(S, E, O, P, tab, gap, X, it);
+#endif
             if (S.stop) {
+                XB_COUNT(4);
                 const int r = S.stop;
                 if (P.pilot) {
                     P.pilot_w[qidx] = r == kEscalate ? -1 : S.delta_w;
@@ -495,6 +522,10 @@ __global__ void __launch_bounds__(kTB, tier_min_blocks<K>()) thread_tier_kernel(
         ++it;
     }
     if (P.pilot) return;
+#if XB_COUNTERS
+    for (int q = 0; q < 5; ++q) atomicAdd(&P.ctr->dbg[q], xb_dbg[q]);
+    // warp-level: iterations in which any lane took the rare path
+#endif
     if (my_units) atomicAdd(&P.ctr->units[P.tier], my_units);
     if (my_cells) atomicAdd(&P.ctr->cells[P.tier], my_cells);
     if (my_esc) atomicAdd(&P.ctr->escalated[P.tier], my_esc);

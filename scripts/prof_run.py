@@ -38,5 +38,5 @@ cells = sum(d["cells_tier"])
 print(f"config {a.config} x{a.scale}: {len(t)} tasks, {cells} cells, start tier {d['start_tier']}, "
       f"tiers ms {[round(x, 3) for x in d['ms_tier']]}, units {d['units_tier']}, escalated {d['escalated']}, "
       f"prep {d['ms_prep']:.2f} ms, pilot {d['ms_pilot']:.2f} ms, "
-      f"GCUPS {cells / (d['ms_total'] / 1e3) / 1e9:.1f}")
+      f"GCUPS {cells / (d['ms_total'] / 1e3) / 1e9:.1f}" + (f" dbg {d['dbg']}" if any(d['dbg']) else ""))
 L.xb_batch_free(b)
