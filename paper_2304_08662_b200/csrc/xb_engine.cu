@@ -859,7 +859,7 @@ static int run_device(xb_batch* B, DevBatch& D) {
                              ? 0 : std::min<long long>(nu, 64 + nu / 512);
     tp.pilot_n = pn;
     tp.pilot_stride = pn ? std::max<long long>(1, nu / pn) : 1;
-    tp.pilot_cap = 4096;
+    tp.pilot_cap = 1024;
     tp.pilot_w = D.d_pilot;
     tp.esc_to_warp = (B->flags & XB_FLAG_ESC_TO_WARP) ? 1 : 0;
     D.mode = mode;
