@@ -8,7 +8,7 @@ CSRC := paper_2304_08662_b200/csrc
 LIB := paper_2304_08662_b200/_lib/libxdrop_b200.so
 OBJDIR := build
 
-SRCS_CU := $(CSRC)/xb_kernels.cu $(CSRC)/xb_thread.cu $(CSRC)/xb_engine.cu
+SRCS_CU := $(CSRC)/xb_kernels.cu $(CSRC)/xb_thread.cu $(CSRC)/xb_group.cu $(CSRC)/xb_engine.cu
 SRCS_CPP := $(CSRC)/xb_synth.cpp
 HDRS := $(CSRC)/xb_internal.h $(CSRC)/xb_kernels.cuh include/xdrop_b200.h
 
@@ -26,6 +26,10 @@ $(OBJDIR)/xb_thread.o: $(CSRC)/xb_thread.cu $(HDRS)
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(NVFLAGS) -dc -o $@ $< 2> $(OBJDIR)/xb_thread.ptxas.txt || (cat $(OBJDIR)/xb_thread.ptxas.txt; exit 1)
 
+$(OBJDIR)/xb_group.o: $(CSRC)/xb_group.cu $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -dc -o $@ $< 2> $(OBJDIR)/xb_group.ptxas.txt || (cat $(OBJDIR)/xb_group.ptxas.txt; exit 1)
+
 $(OBJDIR)/xb_engine.o: $(CSRC)/xb_engine.cu $(HDRS)
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(NVFLAGS) -dc -o $@ $< 2> $(OBJDIR)/xb_engine.ptxas.txt || (cat $(OBJDIR)/xb_engine.ptxas.txt; exit 1)
@@ -34,7 +38,7 @@ $(OBJDIR)/xb_synth.o: $(CSRC)/xb_synth.cpp include/xdrop_b200.h
 	@mkdir -p $(OBJDIR)
 	/usr/bin/g++ -O3 -std=c++17 -fPIC -c -o $@ $<
 
-$(LIB): $(OBJDIR)/xb_kernels.o $(OBJDIR)/xb_thread.o $(OBJDIR)/xb_engine.o $(OBJDIR)/xb_synth.o
+$(LIB): $(OBJDIR)/xb_kernels.o $(OBJDIR)/xb_thread.o $(OBJDIR)/xb_group.o $(OBJDIR)/xb_engine.o $(OBJDIR)/xb_synth.o
 	@mkdir -p $(dir $(LIB))
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^ -lpthread
 

@@ -81,6 +81,8 @@ typedef struct {
 #define XB_FLAG_GENERIC_ONLY 2  /* route every unit to the warp tier (testing) */
 #define XB_FLAG_FORCE_TIER 8    /* start at thread tier (flags >> 8) & 15, no pilot (testing) */
 #define XB_FLAG_ESC_TO_WARP 16  /* units outgrowing the start tier go straight to the warp tier */
+#define XB_FLAG_GROUP 32        /* every thread-tier launch runs as lane groups (testing) */
+#define XB_FLAG_NO_GROUP 64     /* never use lane groups: one thread per unit throughout (ablation) */
 
 /* Per-call device statistics (summed over devices; times are the max).
  * Tiers: 0..4 = one unit per thread with a K = 16/24/32/48/64 slot band,

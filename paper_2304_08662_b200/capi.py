@@ -32,6 +32,8 @@ XB_FLAG_NO_SORT = 1
 XB_FLAG_GENERIC_ONLY = 2
 XB_FLAG_FORCE_TIER = 8
 XB_FLAG_ESC_TO_WARP = 16
+XB_FLAG_GROUP = 32
+XB_FLAG_NO_GROUP = 64
 
 
 def force_tier(t: int) -> int:

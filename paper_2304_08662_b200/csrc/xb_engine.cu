@@ -27,6 +27,8 @@
 namespace xb {
 template <int K, int MODE>
 __global__ void thread_tier_kernel(TierParams P);
+template <int K, int G, int MODE>
+__global__ void group_tier_kernel(TierParams P);
 template <int ENC>
 __global__ void warp_tier_kernel(TierParams P);
 __global__ void select_tier_kernel(TierParams P, int forced);
@@ -566,6 +568,7 @@ struct DevBatch {
     cudaEvent_t* ev = nullptr;
     int sm_count = 0;
     int occ[5] = {0, 0, 0, 0, 0};
+    int gocc[5] = {0, 0, 0, 0, 0};  // lane-group kernels
     int mode = 0;
     int launches = 0;
     // host staging (pinned)
@@ -730,39 +733,43 @@ static int upload_inputs(xb_batch* B, DevBatch& D, const void* items) {
     return XB_OK;
 }
 
-template <int MODE>
-static cudaError_t launch_thread_tier(int t, const TierParams& P, int blocks, cudaStream_t st) {
-    switch (t) {
-        case 0: thread_tier_kernel<16, MODE><<<blocks, kTB, 0, st>>>(P); break;
-        case 1: thread_tier_kernel<24, MODE><<<blocks, kTB, 0, st>>>(P); break;
-        case 2: thread_tier_kernel<32, MODE><<<blocks, kTB, 0, st>>>(P); break;
-        case 3: thread_tier_kernel<48, MODE><<<blocks, kTB, 0, st>>>(P); break;
-        default: thread_tier_kernel<64, MODE><<<blocks, kTB, 0, st>>>(P); break;
-    }
-    return cudaGetLastError();
+constexpr int kGroupLanes = 4;  // lanes per unit in the lane-group tiers
+
+template <bool GROUP, int K, int MODE>
+static void* tier_fn() {
+    if constexpr (GROUP)
+        return reinterpret_cast<void*>(group_tier_kernel<K, kGroupLanes, MODE>);
+    else
+        return reinterpret_cast<void*>(thread_tier_kernel<K, MODE>);
 }
 
-static cudaError_t launch_tier(int mode, int t, const TierParams& P, int blocks, cudaStream_t st) {
-    if (mode == 0) return launch_thread_tier<0>(t, P, blocks, st);
-    if (mode == 1) return launch_thread_tier<1>(t, P, blocks, st);
-    return launch_thread_tier<2>(t, P, blocks, st);
-}
-
-template <int MODE>
-static cudaError_t occ_mode(int t, int* b) {
+template <bool GROUP, int MODE>
+static void* tier_fn_t(int t) {
     switch (t) {
-        case 0: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(b, thread_tier_kernel<16, MODE>, kTB, 0);
-        case 1: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(b, thread_tier_kernel<24, MODE>, kTB, 0);
-        case 2: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(b, thread_tier_kernel<32, MODE>, kTB, 0);
-        case 3: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(b, thread_tier_kernel<48, MODE>, kTB, 0);
-        default: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(b, thread_tier_kernel<64, MODE>, kTB, 0);
+        case 0: return tier_fn<GROUP, 16, MODE>();
+        case 1: return tier_fn<GROUP, 24, MODE>();
+        case 2: return tier_fn<GROUP, 32, MODE>();
+        case 3: return tier_fn<GROUP, 48, MODE>();
+        default: return tier_fn<GROUP, 64, MODE>();
     }
 }
 
-static int occupancy_blocks(int t, int mode, int* out) {
+static void* tier_kernel(bool group, int mode, int t) {
+    if (group) return mode == 0 ? tier_fn_t<true, 0>(t) : mode == 1 ? tier_fn_t<true, 1>(t) : tier_fn_t<true, 2>(t);
+    return mode == 0 ? tier_fn_t<false, 0>(t) : mode == 1 ? tier_fn_t<false, 1>(t) : tier_fn_t<false, 2>(t);
+}
+
+static cudaError_t launch_tier(bool group, int mode, int t, const TierParams& P, int blocks,
+                               cudaStream_t st) {
+    TierParams q = P;
+    void* args[] = {&q};
+    return cudaLaunchKernel(tier_kernel(group, mode, t), dim3(unsigned(blocks)), dim3(kTB), args, 0, st);
+}
+
+static int occupancy_blocks(bool group, int t, int mode, int* out) {
     int b = 0;
-    const cudaError_t e = mode == 0 ? occ_mode<0>(t, &b) : mode == 1 ? occ_mode<1>(t, &b) : occ_mode<2>(t, &b);
-    if (e != cudaSuccess) return XB_E_CUDA;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, tier_kernel(group, mode, t), kTB, 0) != cudaSuccess)
+        return XB_E_CUDA;
     *out = std::max(1, b);
     return XB_OK;
 }
@@ -851,6 +858,8 @@ static int run_device(xb_batch* B, DevBatch& D) {
     tp.r64 = 64;
     tp.one = 1;
     tp.zero = 0;
+    tp.two = 2;
+    tp.ones = 0x01010101u;
     for (int f = 0; f < 16; ++f) tp.mulc[f] = f ? (1u << (32 - 2 * f)) : 0u;
     // pilot: a strided sample of the order, each unit run for at most
     // kPilotCap antidiagonals on the widest thread tier, to measure widths
@@ -863,13 +872,25 @@ static int run_device(xb_batch* B, DevBatch& D) {
     tp.pilot_w = D.d_pilot;
     tp.esc_to_warp = (B->flags & XB_FLAG_ESC_TO_WARP) ? 1 : 0;
     D.mode = mode;
-    for (int t = 0; t < 5; ++t)
-        if (!D.occ[t]) CK(occupancy_blocks(t, mode, &D.occ[t]) ? cudaErrorUnknown : cudaSuccess);
+    // Lane groups (several lanes per unit) finish a unit several times
+    // sooner at ~1.8x the instructions per cell: they take the work whose
+    // wall time is set by per-unit latency, not by throughput -- the pilot,
+    // escalations, and batches too small to fill the SMs with thread units.
+    const bool all_group = (B->flags & XB_FLAG_GROUP) ||
+                           (!(B->flags & XB_FLAG_NO_GROUP) && nu <= int64_t(D.sm_count) * 256);
+    const bool no_group = (B->flags & XB_FLAG_NO_GROUP) && !(B->flags & XB_FLAG_GROUP);
+    for (int t = 0; t < 5; ++t) {
+        if (!D.occ[t]) CK(occupancy_blocks(false, t, mode, &D.occ[t]) ? cudaErrorUnknown : cudaSuccess);
+        if (!D.gocc[t]) CK(occupancy_blocks(true, t, mode, &D.gocc[t]) ? cudaErrorUnknown : cudaSuccess);
+    }
     if (pn > 0) {
         tp.tier = 4;
         tp.pilot = 1;
-        const int blocks = int(std::min<long long>(D.sm_count * D.occ[4], (pn + kTB - 1) / kTB));
-        CK(launch_tier(mode, 4, tp, blocks, D.stream));
+        tp.role = kRoleAll;
+        const bool g = !no_group;
+        const long long lanes = pn * (g ? kGroupLanes : 1);
+        const int blocks = int(std::min<long long>(D.sm_count * (g ? D.gocc[4] : D.occ[4]), (lanes + kTB - 1) / kTB));
+        CK(launch_tier(g, mode, 4, tp, blocks, D.stream));
         ++D.launches;
     }
     tp.pilot = 0;
@@ -880,8 +901,20 @@ static int run_device(xb_batch* B, DevBatch& D) {
     // ---- cascade: the start tier takes the queue, wider tiers their escalations ----
     for (int t = 0; t < 5; ++t) {
         tp.tier = t;
-        CK(launch_tier(mode, t, tp, D.sm_count * D.occ[t], D.stream));
-        ++D.launches;
+        if (all_group || no_group) {
+            tp.role = kRoleAll;
+            CK(launch_tier(all_group, mode, t, tp, D.sm_count * (all_group ? D.gocc[t] : D.occ[t]), D.stream));
+            ++D.launches;
+        } else {
+            tp.role = kRoleStart;
+            CK(launch_tier(false, mode, t, tp, D.sm_count * D.occ[t], D.stream));
+            ++D.launches;
+            if (t > 0) {
+                tp.role = kRoleEscalations;
+                CK(launch_tier(true, mode, t, tp, D.sm_count * D.gocc[t], D.stream));
+                ++D.launches;
+            }
+        }
         CK(cudaEventRecord(D.ev[3 + t], D.stream));
     }
     // ---- warp per unit: exact generic path for whatever is left ----

@@ -60,6 +60,7 @@ struct TierParams {
     int32_t tier;                        // this launch's tier index
     int32_t pilot;                       // 1: run the pilot sample, 0: cascade
     int32_t esc_to_warp;                 // escalations skip the wider thread tiers
+    int32_t role;                        // kRole*: which of the tier's queues this launch serves
     int32_t* __restrict__ warp_scratch;  // warp tier: 2*band ints per warp slot
     // opaque constants: kept in c[]/uniform registers so ptxas cannot fold
     // them into ALU-pipe forms (LEA, LOP3 immediates, SEL)
@@ -67,6 +68,8 @@ struct TierParams {
     int32_t r64;                         // 64
     int32_t one;                         // 1
     int32_t zero;                        // 0
+    int32_t two;                         // 2
+    uint32_t ones;                       // 0x01010101
     uint32_t mulc[16];                   // 2^(32-2f), f = 1..15
 };
 
@@ -161,11 +164,13 @@ struct TState {
     int32_t m, n, hdir, vdir, unit;
     // progress
     int32_t d, ubase, dcap;
-    int32_t ls1, hs1, ls2, hs2;  // lowest/highest live slot of rows d-1, d-2; empty = (kBig, -kBig)
+    // rows d-1 (1) and d-2 (2): highest live slot hs and lr = 32*NM-1 - lowest
+    // live slot; both -1 for an empty row (xb_thread.cu, xstep)
+    int32_t lr1, hs1, lr2, hs2;
     int32_t d_vm, d_lim;         // first d needing matrix masks / any rare-path work
     int32_t stop;                // 0 running, else kDone / kBand / kEscalate
-    int32_t spread;              // observed spread when stop == kBand
-    int32_t T, best_d, best_i, delta_w;
+    int32_t Tc;                  // 64 (T + beta d + 1): the running best in chain units
+    int32_t best_d, best_u, delta_w;  // best cell: antidiagonal, folded diagonal
     int32_t cells;               // <= 64 (n + m + 1): int32 under the prep guard
     // windows
     uint32_t VW[MODE == 0 ? NW : NB];
@@ -193,6 +198,50 @@ struct PrepParams {
     uint32_t* __restrict__ warp_list;
     unsigned long long* __restrict__ warp_len;
 };
+
+// Queue roles of a tier launch: a tier can be served by the thread kernel
+// for its main queue and by the lane-group kernel for its escalations.
+enum : int { kRoleAll = 0, kRoleStart = 1, kRoleEscalations = 2 };
+
+// Work source of a launch.  Pilot: a strided sample of the order.  Cascade:
+// the start tier takes the whole main queue, each wider tier the units
+// escalated into it.
+struct Queue {
+    const uint32_t* q = nullptr;
+    unsigned long long len = 0;
+    unsigned long long* cursor = nullptr;
+    long long stride = 1;
+    __device__ __forceinline__ bool next(uint32_t& unit, long long& idx) {
+        const unsigned long long i = atomicAdd(cursor, 1ull);
+        if (i >= len) return false;
+        idx = (long long)i;
+        unit = q[(long long)i * stride];
+        return true;
+    }
+};
+
+__device__ __forceinline__ bool make_queue(const TierParams& P, Queue& Q) {
+    if (P.pilot) {
+        Q.q = P.order;
+        Q.len = (unsigned long long)P.pilot_n;
+        Q.stride = P.pilot_stride;
+        Q.cursor = &P.ctr->cursor[7];
+        return true;
+    }
+    const int t0 = P.ctr->start_tier;
+    if (P.tier < t0) return false;
+    if (P.role == kRoleStart && P.tier != t0) return false;
+    if (P.role == kRoleEscalations && P.tier == t0) return false;
+    Q.cursor = &P.ctr->cursor[P.tier];
+    if (P.tier == t0) {
+        Q.q = P.order;
+        Q.len = (unsigned long long)P.n_units;
+    } else {
+        Q.q = P.lists + (long long)P.tier * P.n_units;
+        Q.len = P.ctr->list_len[P.tier];
+    }
+    return true;
+}
 
 // outcome of one antidiagonal step
 enum : int { kGo = 0, kDone = 1, kBand = 2, kEscalate = 3 };

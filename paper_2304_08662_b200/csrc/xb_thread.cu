@@ -104,15 +104,14 @@ __device__ __forceinline__ void start_unit(TState<K, MODE>& S, int32_t (&E)[K], 
     S.d = 1;
     S.dcap = P.pilot ? P.pilot_cap : (INT_MAX >> 1);
     S.ubase = -(K / 2);
-    S.ls1 = S.hs1 = K / 2;  // antidiagonal 0: the origin, u = 0
-    S.ls2 = kBig;           // antidiagonal -1: empty
-    S.hs2 = -kBig;
+    S.hs1 = K / 2;  // antidiagonal 0: the origin, u = 0
+    S.lr1 = 32 * TState<K, MODE>::NM - 1 - K / 2;
+    S.hs2 = S.lr2 = -1;  // antidiagonal -1: empty
     S.stop = 0;
-    S.spread = 0;
     set_limits(S);
-    S.T = 0;
+    S.Tc = 64;  // 64 (T + beta d + 1) at d = 0, T = 0
     S.best_d = 0;
-    S.best_i = 0;
+    S.best_u = 0;
     S.delta_w = 1;
     S.cells = 1;
 #pragma unroll
@@ -144,6 +143,20 @@ __device__ __forceinline__ int32_t imad(int32_t a, int32_t b, int32_t c) {
     return r;
 }
 
+// single LOP3s (ptxas otherwise splits a two-constant AND/OR into two)
+template <int LUT>
+__device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(d) : "r"(a), "r"(b), "r"(c), "n"(LUT));
+    return d;
+}
+template <int LUT, uint32_t B>
+__device__ __forceinline__ uint32_t lop3i(uint32_t a, uint32_t c) {
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(d) : "r"(a), "n"(B), "r"(c), "n"(LUT));
+    return d;
+}
+
 // Finishes a slot given its diagonal candidate db and gap sources ln/un:
 // recurrence, key, running best, drop test, dead mask.
 template <int k>
@@ -164,21 +177,17 @@ __device__ __forceinline__ int32_t slot_tail(int32_t db, int32_t ln, int32_t un,
 
 template <int K, int MODE, bool ODD, int k>
 __device__ __forceinline__ void slot(int32_t (&cur)[K], const int32_t (&prv)[K],
-                                     const uint32_t (&Z)[(K + 15) / 16],
+                                     const uint32_t (&Z)[(K + 15) / 16][4],
                                      const TState<K, MODE>& S, const TierParams& P,
                                      const int8_t* __restrict__ tab, SlotCtx& X,
                                      uint32_t (&dm)[(K + 31) / 32]) {
     const int32_t dg = cur[k];
     int32_t db;
     if constexpr (MODE == 0) {
-        constexpr int w = k >> 4, f = k & 15;
-        // t = [match bit at 2f+1][1 at 2f]  ->  (t >> 2f) = 1 + 2*match = sim - 2*gap
-        // (one LOP3: imm & (Z | PAT))
-        const uint32_t t = (3u << (2 * f)) & (Z[w] | P.pat);
-        if constexpr (f == 0)
-            db = dg + int32_t(t);
-        else
-            db = dg + int32_t(__umulhi(t, 1u << (32 - 2 * f)));  // LEA.HI: dg + (t >> 2f)
+        // slot f = 4j + q of word w: byte j of Z[w][q] is 1 + 2*match = sim - 2*gap,
+        // picked out by a one-hot byte weight (IDP.4A, FMA pipe)
+        constexpr int w = k >> 4, f = k & 15, q = f & 3, j = f >> 2;
+        db = __dp4a(int(Z[w][q]), 1 << (8 * j), dg);
     } else {
         constexpr int r = k >> 2, q = k & 3;
         // bytes: v code, h code, 0, 0 (sign-replicate of a code byte < 128)
@@ -200,7 +209,7 @@ __device__ __forceinline__ void slot(int32_t (&cur)[K], const int32_t (&prv)[K],
 
 template <int K, int MODE, bool ODD, int... ks>
 __device__ __forceinline__ void all_slots(std::integer_sequence<int, ks...>, int32_t (&cur)[K],
-                                          const int32_t (&prv)[K], const uint32_t (&Z)[(K + 15) / 16],
+                                          const int32_t (&prv)[K], const uint32_t (&Z)[(K + 15) / 16][4],
                                           const TState<K, MODE>& S, const TierParams& P,
                                           const int8_t* __restrict__ tab, SlotCtx& X,
                                           uint32_t (&dm)[(K + 31) / 32]) {
@@ -208,105 +217,195 @@ __device__ __forceinline__ void all_slots(std::integer_sequence<int, ks...>, int
     (slot<K, MODE, ODD, K - 1 - ks>(cur, prv, Z, S, P, tab, X, dm), ...);
 }
 
+// Where a finished unit's outcome goes: its result row, the next tier's
+// escalation list, or (pilot) the widest window seen.
+struct Sink {
+    uint32_t* esc_list;
+    unsigned long long* esc_len;
+    long long qidx;
+    unsigned long long units, cells, esc;
+};
+
+// Records the outcome of the current unit at the step that decides it (the
+// rest of that loop iteration is dead work nobody reads) and sets S.stop.
+template <int K, int MODE>
+__device__ __forceinline__ void finish_unit(TState<K, MODE>& S, const TierParams& P, int code, int spread,
+                                         Sink& sk, int32_t beta) {
+    S.stop = code;
+    if (P.pilot) {
+        P.pilot_w[sk.qidx] = code == kEscalate ? -1 : S.delta_w;
+        return;
+    }
+    if (code == kEscalate) {
+        const unsigned long long slot = atomicAdd(sk.esc_len, 1ull);
+        sk.esc_list[slot] = uint32_t(S.unit);
+        ++sk.esc;
+        return;
+    }
+    DevResult res;
+    res.cells = S.cells;
+    res.delta_w = S.delta_w;
+    if (code == kBand) {
+        res.score = res.h_ext = res.v_ext = 0;
+        res.status = kStatusBand;
+        res.spread = spread;
+    } else {
+        // Tc = 64 (T + beta d + 1) at the current d; the best cell sits on
+        // antidiagonal best_d, folded diagonal best_u: i = floor(best_d/2) - best_u
+        const int best_i = (S.best_d >> 1) - S.best_u;
+        res.score = (S.Tc >> 6) - beta * S.d - 1;
+        res.h_ext = S.best_d - best_i;
+        res.v_ext = best_i;
+        res.status = kStatusOk;
+        res.spread = 0;
+    }
+    P.results[S.unit] = res;
+    ++sk.units;
+    sk.cells += (unsigned long long)S.cells;
+}
+
+__device__ __forceinline__ int bfind32(uint32_t x) {  // highest set bit, -1 for 0
+    int r;
+    asm("bfind.u32 %0, %1;" : "=r"(r) : "r"(x));
+    return r;
+}
+__device__ __forceinline__ int bfind64(uint64_t x) {
+    int r;
+    asm("bfind.u64 %0, %1;" : "=r"(r) : "l"(x));
+    return r;
+}
+
 // One antidiagonal d.  cur holds d-2 on entry and d on exit, prv holds d-1.
-// A step that finds the unit finished (or failing, or outgrowing K) sets
-// S.stop and keeps going: the rest of the step is harmless dead work, which
-// keeps a single exit test per loop iteration instead of per-path copies.
+// A step that decides the unit (finished, failing, outgrowing K) records the
+// outcome and sets S.stop; the rest of the loop iteration is harmless dead
+// work, which keeps a single exit test per iteration.
+//
+// Live ranges are kept as hs (highest live slot) and lr = KB - ls (KB =
+// 32*NM - 1, ls = lowest live slot), both -1 for an empty row: exactly what
+// bfind returns on the live mask and its bit reversal.  With that encoding
+// the window of row d is one max per side, an empty row is neutral as long
+// as the other row is not, and two empty rows give w <= 0 -- a rare-path
+// trigger like every other exception.
 template <int K, int MODE, bool ODD>
 __device__ __forceinline__ void xstep(TState<K, MODE>& S, int32_t (&cur)[K], int32_t (&prv)[K],
                                       const TierParams& P, const int8_t* __restrict__ tab,
-                                      int32_t gap, int32_t X, unsigned it
+                                      int32_t gap, int32_t X, unsigned it, Sink& sk
 #if XB_COUNTERS
                                       , unsigned long long (&xb_dbg)[8]
 #endif
                                       ) {
     using St = TState<K, MODE>;
+    constexpr int KB = 32 * St::NM - 1;
     XB_COUNT(0);
     const int d = S.d;
+    const int32_t beta = -gap;
+    S.Tc += beta << 6;  // the running best's drift: c_init of row d
     // Reachable window (align.cpp:68-81) in slot space: a gap step from row
     // d-1 reaches slots [ls1-1, hs1] (d odd) or [ls1, hs1+1] (d even), a
-    // diagonal step from d-2 the same slots.  Empty rows are [kBig, -kBig].
-    int s_lo = ODD ? min(S.ls1 - 1, S.ls2) : min(S.ls1, S.ls2);
-    int s_hi = ODD ? max(S.hs1, S.hs2) : max(S.hs1 + 1, S.hs2);
-    const int fd = d >> 1;
-    int A = fd - S.ubase;  // slot k holds i = A - k
-    // clamp to the matrix: i <= min(d, n)  and  i >= max(d - m, 0)
-    int w = min(s_hi, A - max(d - S.m, 0)) - max(s_lo, A - min(d, S.n)) + 1;
+    // diagonal step from d-2 the same slots.  Below d_vm the band lies inside
+    // the matrix, so the clamps of align.cpp:80-81 cannot bind.
+    const int M = ODD ? max(S.lr1 + 1, S.lr2) : max(S.lr1, S.lr2);  // KB - s_lo
+    const int s_hi = ODD ? max(S.hs1, S.hs2) : max(S.hs1 + 1, S.hs2);
+    int wm1 = s_hi + M - KB;  // w - 1
     uint32_t vm[St::NM];
 #pragma unroll
     for (int q = 0; q < St::NM; ++q) vm[q] = range_bits(0, min(K - 1 - 32 * q, 31));
-    [[maybe_unused]] uint32_t vms[St::NW];
+    [[maybe_unused]] uint32_t inv[St::NW];  // both bits of slots outside the matrix
 #pragma unroll
-    for (int ww = 0; ww < St::NW; ++ww) vms[ww] = 0xAAAAAAAAu;
+    for (int ww = 0; ww < St::NW; ++ww) inv[ww] = P.zero;
     // one rarely-taken branch for every way a step can stop, reshape or mask
-    if ((s_lo < 0 || unsigned(s_hi) > unsigned(K - 1) || w > P.band || d >= S.d_lim) && !S.stop) {
+    if ((M > KB || unsigned(s_hi) > unsigned(K - 1) || unsigned(wm1) >= unsigned(P.band) ||
+         d >= S.d_lim) && !S.stop) {
         XB_COUNT(1);
-        if (s_hi < 0 || d > S.n + S.m + 1 || d > S.dcap) {
-            S.stop = kDone;  // align.cpp:64-66
-        } else if (w > P.band) {  // align.cpp:93-94: first overflow, cells so far
-            S.stop = kBand;
-            S.spread = w;
+        const bool e1 = S.hs1 < 0, e2 = S.hs2 < 0;
+        if ((e1 && e2) || d > S.n + S.m + 1 || d > S.dcap) {
+            finish_unit(S, P, kDone, 0, sk, beta);  // align.cpp:61-66
         } else {
-            if (s_lo < 0 || s_hi > K - 1) {
-                // every live source lies inside the unclamped window, so it must fit
-                const int wu = s_hi - s_lo + 1;
-                if (wu > K) {
-                    S.stop = kEscalate;
-                } else {
-                    XB_COUNT(3);
-                    const int sh = s_lo - ((K - wu) >> 1);  // new slot 0 = old slot sh
-                    shift_slots<K>(cur, sh);
-                    shift_slots<K>(prv, sh);
-                    S.ubase += sh;
-                    S.ls1 -= sh;
-                    S.hs1 -= sh;
-                    S.ls2 -= sh;
-                    S.hs2 -= sh;
-                    A -= sh;
-                    set_limits(S);
-                    // symbols left to consume before the next refill (iteration multiple
-                    // of 16): this iteration's own consumption counts unless it happened
-                    const int to_refill = 16 - int(it & 15);
-                    init_windows(S, P.pool, ODD ? to_refill : to_refill - 1, to_refill);
-                }
+            int lo = kBig, hi = -kBig;
+            if (!e1) {
+                lo = KB - S.lr1 - (ODD ? 1 : 0);
+                hi = S.hs1 + (ODD ? 0 : 1);
             }
-            if (d >= S.d_vm) {
-                XB_COUNT(2);
-                // slots inside the matrix: i <= n  <=>  k >= klo ;  j <= m  <=>  k <= khi
-                const int klo = A - S.n;
-                const int khi = S.m - (d - fd) - S.ubase;
-                const int khk = min(khi, K - 1);
-#pragma unroll
-                for (int q = 0; q < St::NM; ++q)
-                    vm[q] = range_bits(max(klo - 32 * q, 0), min(khk - 32 * q, 31));
-#pragma unroll
-                for (int ww = 0; ww < St::NW; ++ww) {
-                    const int l = max(klo - 16 * ww, 0), h = min(khi - 16 * ww, 15);
-                    vms[ww] = range_bits(2 * l, 2 * h + 1) & 0xAAAAAAAAu;
+            if (!e2) {
+                lo = min(lo, KB - S.lr2);
+                hi = max(hi, S.hs2);
+            }
+            const int fd = d >> 1;
+            int A = fd - S.ubase;  // slot k holds i = A - k
+            // clamp to the matrix: i <= min(d, n)  and  i >= max(d - m, 0)
+            const int w = min(hi, A - max(d - S.m, 0)) - max(lo, A - min(d, S.n)) + 1;
+            if (w > P.band) {  // align.cpp:93-94: first overflow, cells so far
+                finish_unit(S, P, kBand, w, sk, beta);
+            } else {
+                if (lo < 0 || hi > K - 1) {
+                    // every live source lies inside the unclamped window, so it must fit
+                    const int wu = hi - lo + 1;
+                    if (wu > K) {
+                        finish_unit(S, P, kEscalate, 0, sk, beta);
+                    } else {
+                        XB_COUNT(3);
+                        const int sh = lo - ((K - wu) >> 1);  // new slot 0 = old slot sh
+                        shift_slots<K>(cur, sh);
+                        shift_slots<K>(prv, sh);
+                        S.ubase += sh;
+                        if (!e1) {
+                            S.hs1 -= sh;
+                            S.lr1 += sh;
+                        }
+                        if (!e2) {
+                            S.hs2 -= sh;
+                            S.lr2 += sh;
+                        }
+                        A -= sh;
+                        set_limits(S);
+                        // symbols left to consume before the next refill (iteration multiple
+                        // of 16): this iteration's own consumption counts unless it happened
+                        const int to_refill = 16 - int(it & 15);
+                        init_windows(S, P.pool, ODD ? to_refill : to_refill - 1, to_refill);
+                    }
                 }
+                if (!S.stop && d >= S.d_vm) {
+                    XB_COUNT(2);
+                    // slots inside the matrix: i <= n  <=>  k >= klo ;  j <= m  <=>  k <= khi
+                    const int klo = A - S.n;
+                    const int khi = S.m - (d - fd) - S.ubase;
+                    const int khk = min(khi, K - 1);
+#pragma unroll
+                    for (int q = 0; q < St::NM; ++q)
+                        vm[q] = range_bits(max(klo - 32 * q, 0), min(khk - 32 * q, 31));
+#pragma unroll
+                    for (int ww = 0; ww < St::NW; ++ww) {
+                        const int l = max(klo - 16 * ww, 0), h = min(khi - 16 * ww, 15);
+                        inv[ww] = ~range_bits(2 * l, 2 * h + 1);
+                    }
+                }
+                wm1 = max(w, 0) - 1;  // a clamped-empty row counts no cells (align.cpp:84-90)
             }
         }
     }
-    if (!S.stop) {
-        S.cells += max(w, 0);
-        S.delta_w = max(S.delta_w, w);
-    }
+    S.cells += wm1 + 1;
+    S.delta_w = max(S.delta_w, wm1 + 1);
 
-    // DNA +1/-1/-1: Z[w] bit 2f+1 = slot 16w+f is a match inside the matrix
-    // (one LOP3: ~(x | x << 1) & validity)
-    uint32_t Z[St::NW];
+    // DNA +1/-1/-1: bit 2f+1 of z = ~(x | x << 1), x = (VW ^ HW) | inv, says
+    // slot 16w+f is a match inside the matrix; Z[w][q] moves the bits of slots
+    // f = 4j + q to bit 1 of byte j and sets bit 0: byte j = 1 + 2*match.
+    // 6 ALU (LOP3) + 4 FMA (IMAD) per 16 slots.
+    uint32_t Z[St::NW][4];
     if constexpr (MODE == 0) {
 #pragma unroll
         for (int ww = 0; ww < St::NW; ++ww) {
-            const uint32_t x = S.VW[ww] ^ S.HW[ww];
-            Z[ww] = ~(x | (x << 1)) & vms[ww];
+            const uint32_t x = lop3<0xBE>(S.VW[ww], S.HW[ww], inv[ww]);  // (a ^ b) | c
+            const uint32_t z = lop3<0x03>(x, uint32_t(imad(int32_t(x), P.two, P.zero)), P.zero);  // ~(a | b)
+            Z[ww][0] = lop3i<0xEA, 0x02020202u>(z, P.ones);  // (a & b) | c
+#pragma unroll
+            for (int q = 1; q < 4; ++q)  // z >> 2q on the FMA pipe
+                Z[ww][q] = lop3i<0xEA, 0x02020202u>(__umulhi(z, P.mulc[q]), P.ones);
         }
     }
 
     // exact running best + drop test: chain over k = K-1..0 (ascending i)
-    const int32_t beta = -gap;
     SlotCtx C;
-    C.c = (S.T + beta * d + 1) << 6;  // (T + beta d + off - X) * 64
+    C.c = S.Tc;  // (T + beta d + off - X) * 64
     C.negC = -((X << 6) + 63);
     C.r64 = P.r64;
     C.one = P.one;
@@ -316,36 +415,27 @@ __device__ __forceinline__ void xstep(TState<K, MODE>& S, int32_t (&cur)[K], int
     for (int q = 0; q < St::NM; ++q) dm[q] = 0u;
     all_slots<K, MODE, ODD>(std::make_integer_sequence<int, K>{}, cur, prv, Z, S, P, tab, C, dm);
 
-    // running best (align.cpp:123-127): strict improvement, first slot wins
-    {
-        const int32_t cf = C.c + ((X << 6) + 63);
-        const int32_t qnew = cf >> 6;
-        const int32_t qold = S.T + beta * d + X + 1;
-        if (qnew > qold && !S.stop) {
-            S.T = qnew - beta * d - X - 1;
-            S.best_d = d;
-            S.best_i = A - (cf & 63);
-        }
+    // running best (align.cpp:123-127): strict improvement, first slot wins.
+    // The chain ends above its start exactly when some cell beat T; then
+    // (c + 63) rounds up to the new 64 (T' + beta d + 1) and its low bits are
+    // the first attaining slot.
+    if (C.c != S.Tc) {
+        const int32_t c63 = C.c + 63;
+        S.Tc = c63 & ~63;
+        S.best_d = d;
+        S.best_u = S.ubase + (c63 & 63);
     }
     // live slots of row d (align.cpp:138-145); out-of-matrix slots masked
-    {
-        int hs, ls;
-        bool any;
-        if constexpr (St::NM == 1) {
-            const uint32_t lv = ~dm[0] & vm[0];
-            any = lv != 0u;
-            hs = 31 - __clz(lv);
-            ls = __ffs(lv) - 1;
-        } else {
-            const uint32_t lv0 = ~dm[0] & vm[0], lv1 = ~dm[1] & vm[1];
-            any = (lv0 | lv1) != 0u;
-            hs = lv1 ? 63 - __clz(lv1) : 31 - __clz(lv0);
-            ls = lv0 ? __ffs(lv0) - 1 : 31 + __ffs(lv1);
-        }
-        S.ls2 = S.ls1;
-        S.hs2 = S.hs1;
-        S.ls1 = any ? ls : kBig;
-        S.hs1 = any ? hs : -kBig;
+    S.hs2 = S.hs1;
+    S.lr2 = S.lr1;
+    if constexpr (St::NM == 1) {
+        const uint32_t lv = ~dm[0] & vm[0];
+        S.hs1 = bfind32(lv);
+        S.lr1 = bfind32(__brev(lv));
+    } else {
+        const uint64_t lv = (uint64_t(~dm[1] & vm[1]) << 32) | (~dm[0] & vm[0]);
+        S.hs1 = bfind64(lv);
+        S.lr1 = bfind64(__brevll(lv));
     }
 
     // feed the symbol that enters the band on d+1
@@ -357,7 +447,7 @@ __device__ __forceinline__ void xstep(TState<K, MODE>& S, int32_t (&cur)[K], int
             S.rv.cur <<= 2;
         } else {
             constexpr int ENC = MODE == 1 ? ENC_2BIT : ENC_5BIT;
-            const uint32_t code = code_at<ENC>(P.pool, S.v_pos, S.vdir, S.n, int64_t(fd) - S.ubase);
+            const uint32_t code = code_at<ENC>(P.pool, S.v_pos, S.vdir, S.n, int64_t(d >> 1) - S.ubase);
 #pragma unroll
             for (int r = St::NB - 1; r > 0; --r) S.VW[r] = __funnelshift_l(S.VW[r - 1], S.VW[r], 8);
             S.VW[0] = (S.VW[0] << 8) | code;
@@ -371,51 +461,13 @@ __device__ __forceinline__ void xstep(TState<K, MODE>& S, int32_t (&cur)[K], int
         } else {
             constexpr int ENC = MODE == 1 ? ENC_2BIT : ENC_5BIT;
             const uint32_t code =
-                code_at<ENC>(P.pool, S.h_pos, S.hdir, S.m, int64_t(d - fd) + S.ubase - 1 + St::WK);
+                code_at<ENC>(P.pool, S.h_pos, S.hdir, S.m, int64_t(d - (d >> 1)) + S.ubase - 1 + St::WK);
 #pragma unroll
             for (int r = 0; r < St::NB - 1; ++r) S.HW[r] = __funnelshift_r(S.HW[r], S.HW[r + 1], 8);
             S.HW[St::NB - 1] = __funnelshift_r(S.HW[St::NB - 1], code, 8);
         }
     }
     S.d = d + 1;
-}
-
-// Work source of a launch.  Pilot: a strided sample of the order.  Cascade:
-// the start tier takes the whole main queue, each wider tier the units
-// escalated into it.
-struct Queue {
-    const uint32_t* q = nullptr;
-    unsigned long long len = 0;
-    unsigned long long* cursor = nullptr;
-    long long stride = 1;
-    __device__ __forceinline__ bool next(uint32_t& unit, long long& idx) {
-        const unsigned long long i = atomicAdd(cursor, 1ull);
-        if (i >= len) return false;
-        idx = (long long)i;
-        unit = q[(long long)i * stride];
-        return true;
-    }
-};
-
-__device__ __forceinline__ bool make_queue(const TierParams& P, Queue& Q) {
-    if (P.pilot) {
-        Q.q = P.order;
-        Q.len = (unsigned long long)P.pilot_n;
-        Q.stride = P.pilot_stride;
-        Q.cursor = &P.ctr->cursor[7];
-        return true;
-    }
-    const int t0 = P.ctr->start_tier;
-    if (P.tier < t0) return false;
-    Q.cursor = &P.ctr->cursor[P.tier];
-    if (P.tier == t0) {
-        Q.q = P.order;
-        Q.len = (unsigned long long)P.n_units;
-    } else {
-        Q.q = P.lists + (long long)P.tier * P.n_units;
-        Q.len = P.ctr->list_len[P.tier];
-    }
-    return true;
 }
 
 // resident blocks per SM the register budget is sized for
@@ -442,9 +494,11 @@ __global__ void __launch_bounds__(kTB, tier_min_blocks<K>()) thread_tier_kernel(
         __syncthreads();
     }
     const int next_tier = P.esc_to_warp ? kWarpTier : P.tier + 1;
-    uint32_t* esc_list = P.lists + (long long)next_tier * P.n_units;
-    unsigned long long* esc_len = &P.ctr->list_len[next_tier];
-    unsigned long long my_units = 0, my_cells = 0, my_esc = 0;
+    Sink sk;
+    sk.esc_list = P.lists + (long long)next_tier * P.n_units;
+    sk.esc_len = &P.ctr->list_len[next_tier];
+    sk.qidx = 0;
+    sk.units = sk.cells = sk.esc = 0;
 #if XB_COUNTERS
     unsigned long long xb_dbg[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #endif
@@ -452,17 +506,16 @@ __global__ void __launch_bounds__(kTB, tier_min_blocks<K>()) thread_tier_kernel(
     TState<K, MODE> S;
     int32_t E[K], O[K];
     bool active = false;
-    long long qidx = 0;
     // warp-uniform iteration counter (2 antidiagonals each); the first units
     // start "at the end of iteration -1"
     unsigned it = 0xFFFFFFFFu;
     auto fetch = [&]() {
         active = false;
         uint32_t unit;
-        while (Q.next(unit, qidx)) {
+        while (Q.next(unit, sk.qidx)) {
             // units whose values could leave the drift-space range go to the warp tier
             if (P.units[unit].route != 0) {
-                if (P.pilot) P.pilot_w[qidx] = -2;  // not a thread-tier unit
+                if (P.pilot) P.pilot_w[sk.qidx] = -2;  // not a thread-tier unit
                 continue;
             }
             start_unit<K, MODE>(S, E, O, P, unit, X, it);
@@ -482,40 +535,14 @@ __global__ void __launch_bounds__(kTB, tier_min_blocks<K>()) thread_tier_kernel(
                 }
             }
 #if XB_COUNTERS
-            xstep<K, MODE, true>(S, O, E, P, tab, gap, X, it, xb_dbg);
-            xstep<K, MODE, false>(S, E, O, P, tab, gap, X, it, xb_dbg);
+            xstep<K, MODE, true>(S, O, E, P, tab, gap, X, it, sk, xb_dbg);
+            xstep<K, MODE, false>(S, E, O, P, tab, gap, X, it, sk, xb_dbg);
 #else
-            xstep<K, MODE, true>(S, O, E, P, tab, gap, X, it);
-            xstep<K, MODE, false>(S, E, O, P, tab, gap, X, it);
+            xstep<K, MODE, true>(S, O, E, P, tab, gap, X, it, sk);
+            xstep<K, MODE, false>(S, E, O, P, tab, gap, X, it, sk);
 #endif
-            if (S.stop) {
+            if (S.stop) {  // outcome already recorded by the deciding step
                 XB_COUNT(4);
-                const int r = S.stop;
-                if (P.pilot) {
-                    P.pilot_w[qidx] = r == kEscalate ? -1 : S.delta_w;
-                } else if (r == kEscalate) {
-                    const unsigned long long slot = atomicAdd(esc_len, 1ull);
-                    esc_list[slot] = uint32_t(S.unit);
-                    ++my_esc;
-                } else {
-                    DevResult res;
-                    res.cells = S.cells;
-                    res.delta_w = S.delta_w;
-                    if (r == kBand) {
-                        res.score = res.h_ext = res.v_ext = 0;
-                        res.status = kStatusBand;
-                        res.spread = S.spread;
-                    } else {
-                        res.score = S.T;
-                        res.h_ext = S.best_d - S.best_i;
-                        res.v_ext = S.best_i;
-                        res.status = kStatusOk;
-                        res.spread = 0;
-                    }
-                    P.results[S.unit] = res;
-                    ++my_units;
-                    my_cells += (unsigned long long)S.cells;
-                }
                 fetch();
             }
         }
@@ -524,11 +551,10 @@ __global__ void __launch_bounds__(kTB, tier_min_blocks<K>()) thread_tier_kernel(
     if (P.pilot) return;
 #if XB_COUNTERS
     for (int q = 0; q < 5; ++q) atomicAdd(&P.ctr->dbg[q], xb_dbg[q]);
-    // warp-level: iterations in which any lane took the rare path
 #endif
-    if (my_units) atomicAdd(&P.ctr->units[P.tier], my_units);
-    if (my_cells) atomicAdd(&P.ctr->cells[P.tier], my_cells);
-    if (my_esc) atomicAdd(&P.ctr->escalated[P.tier], my_esc);
+    if (sk.units) atomicAdd(&P.ctr->units[P.tier], sk.units);
+    if (sk.cells) atomicAdd(&P.ctr->cells[P.tier], sk.cells);
+    if (sk.esc) atomicAdd(&P.ctr->escalated[P.tier], sk.esc);
 }
 
 #define XB_INST(K)                                                   \

@@ -54,8 +54,13 @@ def _by_scheme(entries):
     return groups
 
 
-TIER_FLAGS = [0, 2] + [8 | (t << 8) for t in range(5)]
-TIER_IDS = ["pilot_cascade", "warp_tier_only", "k16", "k24", "k32", "k48", "k64"]
+# 64 = NO_GROUP (one thread per unit), 32 = GROUP (lane groups throughout),
+# 8 | t << 8 = start at tier t without the pilot
+TIER_FLAGS = ([0, 2, 64] + [64 | 8 | (t << 8) for t in range(5)]
+              + [32 | 8 | (t << 8) for t in range(5)])
+TIER_IDS = (["auto", "warp_tier_only", "thread_pilot_cascade"]
+            + [f"thread_k{w}" for w in (16, 24, 32, 48, 64)]
+            + [f"group_k{w}" for w in (16, 24, 32, 48, 64)])
 
 
 @pytest.mark.parametrize("flags", TIER_FLAGS, ids=TIER_IDS)
@@ -134,8 +139,9 @@ def _config_pool(xb, ds):
 
 
 @pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
-@pytest.mark.parametrize("flags", [0, 1, 2, 8 | (0 << 8), 8 | (2 << 8)],
-                         ids=["cascade", "unsorted", "warp_tier_only", "from_k16", "from_k32"])
+@pytest.mark.parametrize("flags", [0, 1, 2, 64, 32, 64 | 8, 64 | 8 | (2 << 8), 32 | 8, 32 | 8 | (2 << 8)],
+                         ids=["auto", "unsorted", "warp_tier_only", "thread_cascade", "group_cascade",
+                              "thread_from_k16", "thread_from_k32", "group_from_k16", "group_from_k32"])
 def test_configs_vs_reference_golden(xb, cfg, flags):
     from paper_2304_08662_b200 import synth
     meta = load_json("configs_meta.json")[str(cfg)]
@@ -167,8 +173,9 @@ def test_configs_sample_vs_oracle_full_size(xb, oracle, cfg):
     assert result_rows_equal(out, exp).all()
     assert (ss == ess).all()
     a, _ = xb.extend_tasks(pool, ds.tasks, ds.k, ds.band)
-    b, _ = xb.extend_tasks(pool, ds.tasks, ds.k, ds.band, exec_flags=1)
-    assert result_rows_equal(a, b).all()
+    for flags in (1, 32, 64):  # unsorted, lane groups throughout, one thread per unit
+        b, _ = xb.extend_tasks(pool, ds.tasks, ds.k, ds.band, exec_flags=flags)
+        assert result_rows_equal(a, b).all(), flags
     # every sampled row inside the full run equals the sampled run
     full = a.reshape(-1, 2)[pick].reshape(-1)
     assert result_rows_equal(full, out).all()
@@ -208,7 +215,8 @@ def test_self_extension_full_length(xb):
     assert len(set(right["delta_w"].tolist())) == 1
 
 
-def test_band_failures_and_escalation(xb, oracle):
+@pytest.mark.parametrize("flags", [0, 32, 64, 64 | 8], ids=["auto", "group", "thread", "thread_from_k16"])
+def test_band_failures_and_escalation(xb, oracle, flags):
     """Wide windows: X large so spreads exceed 32 and 64 slots (tier escalation)
     and a band small enough that some sides fail with exact spread/cells."""
     rng = random.Random(7)
@@ -232,7 +240,7 @@ def test_band_failures_and_escalation(xb, oracle):
         for q, (h, v) in enumerate(entries):
             units[q] = (2 * q, 2 * q + 1, 1, 1, 0, 0, len(h), len(v))
         pool = xb.DevicePool(xb.ScoringScheme.match_mismatch(1, -1, -1, x), sym, np.array(off))
-        out = xb.extend_units(pool, units, band)
+        out = xb.extend_units(pool, units, band, exec_flags=flags)
         for q, (h, v) in enumerate(entries):
             assert rec_tuple(out[q]) == rec_tuple(oracle.extend(h, v, so, band)), (x, band, q)
 
