@@ -34,6 +34,7 @@ XB_FLAG_FORCE_TIER = 8
 XB_FLAG_ESC_TO_WARP = 16
 XB_FLAG_GROUP = 32
 XB_FLAG_NO_GROUP = 64
+XB_FLAG_THROUGHPUT = 128
 
 
 def force_tier(t: int) -> int:

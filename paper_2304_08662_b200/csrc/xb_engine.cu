@@ -486,6 +486,7 @@ struct Workspace {
     uint32_t* d_lists = nullptr;
     DevCounters* d_ctr = nullptr;
     int32_t* d_scratch = nullptr;
+    int32_t* d_resume = nullptr;  // kResumeCap escalation records
     int32_t* d_pilot = nullptr;
     void* d_cub = nullptr;
     DevResult* h_res = nullptr;
@@ -529,6 +530,7 @@ struct Workspace {
         release_items();
         cudaFree(d_ctr);
         cudaFree(d_scratch);
+        cudaFree(d_resume);
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
         if (stream) cudaStreamDestroy(stream);
@@ -561,6 +563,7 @@ struct DevBatch {
     uint32_t* d_lists = nullptr;  // kNumTiers x n_units escalation inputs
     DevCounters* d_ctr = nullptr;
     int32_t* d_scratch = nullptr;
+    int32_t* d_resume = nullptr;
     int32_t* d_pilot = nullptr;
     int scratch_warps = 0;
     void* d_cub = nullptr;
@@ -637,6 +640,7 @@ static int setup_device(xb_batch* B, DevBatch& D, const xb_exec* ex) {
         CK(cudaStreamCreateWithFlags(&W.stream, cudaStreamNonBlocking));
         for (auto& e : W.ev) CK(cudaEventCreate(&e));
         CK(cudaMalloc(&W.d_ctr, sizeof(DevCounters)));
+        CK(cudaMalloc(&W.d_resume, size_t(kResumeCap) * kResumeStride * 4));
     }
     D.stream = (ex && ex->stream && B->devs.size() == 1) ? (cudaStream_t)ex->stream : W.stream;
     D.ev = W.ev;
@@ -695,6 +699,7 @@ static int setup_device(xb_batch* B, DevBatch& D, const xb_exec* ex) {
     D.d_cub = W.d_cub;
     D.cub_bytes = W.cub_bytes;
     D.d_scratch = W.d_scratch;
+    D.d_resume = W.d_resume;
     D.h_res = W.h_res;
     D.d_tasks = W.d_tasks;
     D.d_seed = W.d_seed;
@@ -854,6 +859,7 @@ static int run_device(xb_batch* B, DevBatch& D) {
     tp.n_units = nu;
     tp.band = B->band;
     tp.warp_scratch = D.d_scratch;
+    tp.resume = D.d_resume;
     tp.pat = 0x55555555u;
     tp.r64 = 64;
     tp.one = 1;
@@ -861,24 +867,28 @@ static int run_device(xb_batch* B, DevBatch& D) {
     tp.two = 2;
     tp.ones = 0x01010101u;
     for (int f = 0; f < 16; ++f) tp.mulc[f] = f ? (1u << (32 - 2 * f)) : 0u;
-    // pilot: a strided sample of the order, each unit run for at most
-    // kPilotCap antidiagonals on the widest thread tier, to measure widths
     const int forced = (B->flags & XB_FLAG_FORCE_TIER) ? ((B->flags >> 8) & 15) : -1;
-    const long long pn = (forced >= 0 || (B->flags & XB_FLAG_GENERIC_ONLY))
-                             ? 0 : std::min<long long>(nu, 64 + nu / 512);
-    tp.pilot_n = pn;
-    tp.pilot_stride = pn ? std::max<long long>(1, nu / pn) : 1;
-    tp.pilot_cap = 1024;
-    tp.pilot_w = D.d_pilot;
-    tp.esc_to_warp = (B->flags & XB_FLAG_ESC_TO_WARP) ? 1 : 0;
     D.mode = mode;
     // Lane groups (several lanes per unit) finish a unit several times
     // sooner at ~1.8x the instructions per cell: they take the work whose
     // wall time is set by per-unit latency, not by throughput -- the pilot,
     // escalations, and batches too small to fill the SMs with thread units.
-    const bool all_group = (B->flags & XB_FLAG_GROUP) ||
-                           (!(B->flags & XB_FLAG_NO_GROUP) && nu <= int64_t(D.sm_count) * 256);
+    const bool latency_mode = nu <= int64_t(D.sm_count) * 256 && !(B->flags & XB_FLAG_THROUGHPUT);
+    const bool all_group = (B->flags & XB_FLAG_GROUP) || (!(B->flags & XB_FLAG_NO_GROUP) && latency_mode);
     const bool no_group = (B->flags & XB_FLAG_NO_GROUP) && !(B->flags & XB_FLAG_GROUP);
+    // pilot: a strided sample of the order, each unit run for at most
+    // pilot_cap antidiagonals on the widest thread tier, to measure widths.
+    // A latency-bound batch skips it: the pilot would cost about as much as
+    // the batch, and there a start a little too wide (K32) costs far less
+    // than an escalation, which re-runs the unit after the whole start tier.
+    const long long pn = (forced >= 0 || (B->flags & XB_FLAG_GENERIC_ONLY) || latency_mode)
+                             ? 0 : std::min<long long>(nu, 64 + nu / 512);
+    const int default_start = latency_mode ? 2 : 4;
+    tp.pilot_n = pn;
+    tp.pilot_stride = pn ? std::max<long long>(1, nu / pn) : 1;
+    tp.pilot_cap = 1024;
+    tp.pilot_w = D.d_pilot;
+    tp.esc_to_warp = (B->flags & XB_FLAG_ESC_TO_WARP) ? 1 : 0;
     for (int t = 0; t < 5; ++t) {
         if (!D.occ[t]) CK(occupancy_blocks(false, t, mode, &D.occ[t]) ? cudaErrorUnknown : cudaSuccess);
         if (!D.gocc[t]) CK(occupancy_blocks(true, t, mode, &D.gocc[t]) ? cudaErrorUnknown : cudaSuccess);
@@ -894,7 +904,7 @@ static int run_device(xb_batch* B, DevBatch& D) {
         ++D.launches;
     }
     tp.pilot = 0;
-    select_tier_kernel<<<1, 32, 0, D.stream>>>(tp, forced >= 0 ? forced : (pn > 0 ? -1 : 4));
+    select_tier_kernel<<<1, 32, 0, D.stream>>>(tp, forced >= 0 ? forced : (pn > 0 ? -1 : default_start));
     CK(cudaGetLastError());
     ++D.launches;
     CK(cudaEventRecord(D.ev[2], D.stream));

@@ -1,18 +1,20 @@
 // Lane-group tiers: G lanes of a warp cooperate on one unit, each holding
-// S = K/G consecutive slots of the register band.  Same exact semantics as
-// the thread tier (xb_thread.cu, proofs in xb_kernels.cuh); what changes is
-// the plumbing between slots that live in different lanes:
+// S = K/G consecutive slots of the register band.  Same exact semantics and
+// bookkeeping as the thread tier (xb_thread.cu; coordinates and proofs in
+// xb_kernels.cuh); what changes is the plumbing between slots that live in
+// different lanes:
 //   * the one gap source that crosses a lane edge comes by SHFL (up on even
 //     antidiagonals, down on odd ones), and so do the symbols entering a
 //     lane's window;
 //   * the running-best chain, which runs over slots in descending order,
-//     becomes: lane-local key maximum -> exclusive suffix-max across the
-//     group (log2 G shuffles) -> lane-local chain seeded with it;
-//   * the live range is an OR-butterfly of the lanes' live bits.
-// A step then costs ~S slots of dependent work plus a few shuffle rounds
-// instead of K slots, so a unit advances several times faster: this tier
-// serves work that is latency- rather than throughput-bound (escalation
-// tails, the pilot, and batches too small to fill the machine).
+//     becomes: lane-local key maximum -> one all-gather round (G independent
+//     shuffles) giving each lane the maximum of the higher lanes and the
+//     group maximum -> lane-local chain seeded with it;
+//   * the live range is a second all-gather round of the lanes' live bits.
+// A step then costs ~S slots of dependent work plus two shuffle rounds on
+// its critical path instead of K slots: this tier serves work that is
+// latency- rather than throughput-bound (escalation tails, the pilot, and
+// batches too small to fill the machine).
 #include <climits>
 #include <cstdint>
 #include <utility>
@@ -28,17 +30,35 @@ __device__ __forceinline__ uint32_t gbits(int lo, int hi) {
     return (0xFFFFFFFFu >> (31 - hi)) & (0xFFFFFFFFu << lo);
 }
 
+__device__ __forceinline__ int gbfind32(uint32_t x) {
+    int r;
+    asm("bfind.u32 %0, %1;" : "=r"(r) : "r"(x));
+    return r;
+}
+__device__ __forceinline__ int gbfind64(uint64_t x) {
+    int r;
+    asm("bfind.u64 %0, %1;" : "=r"(r) : "l"(x));
+    return r;
+}
+template <int LUT>
+__device__ __forceinline__ uint32_t glop3(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(d) : "r"(a), "r"(b), "r"(c), "n"(LUT));
+    return d;
+}
+
 template <int K, int G, int MODE>
 struct GState {
     static constexpr int S = K / G;          // slots per lane
     static constexpr int NB = (S + 3) / 4;   // byte-window words per lane (table mode)
     static constexpr int NM = (K + 31) / 32; // group live-mask words
+    static constexpr int KB = 32 * NM - 1;
     int64_t h_pos, v_pos;
     int32_t m, n, hdir, vdir, unit;
     int32_t d, ubase, dcap;
-    int32_t ls1, hs1, ls2, hs2;  // global slots, empty = (kBig, -kBig)
-    int32_t d_vm, d_lim, stop, spread;
-    int32_t T, best_d, best_i, delta_w, cells;
+    int32_t lr1, hs1, lr2, hs2;  // group slots; hs / KB - ls, -1 for an empty row
+    int32_t d_vm, d_lim, stop;
+    int32_t Tc, best_d, best_u, cells, delta_w;
     uint32_t VW, HW;             // 2-bit windows of this lane's S slots (MODE 0)
     uint32_t VWb[NB], HWb[NB];   // byte windows (table modes)
     Reader<true> rv;             // lane 0: v symbols entering slot 0
@@ -100,182 +120,25 @@ __device__ __forceinline__ void g_shift1(int32_t (&R)[SS], int dir, int lane, un
     }
 }
 
+struct GSink {
+    uint32_t* esc_list;
+    unsigned long long* esc_len;
+    long long qidx;
+    unsigned long long units, cells, esc;
+    bool resumable;
+};
+
 }  // namespace
 
-template <int K, int G, int MODE, bool ODD>
-__device__ __forceinline__ void gstep(GState<K, G, MODE>& S, int32_t (&cur)[K / G],
-                                      int32_t (&prv)[K / G], const TierParams& P,
-                                      const int8_t* __restrict__ tab, int32_t gap, int32_t X,
-                                      unsigned it, int lane, unsigned gmask) {
+// Symbols entering on d+1 (v after an odd step, h after an even one).
+// FM: the whole warp executes this call (full-mask shuffles, no convergence
+// check); otherwise only this group does.
+template <int K, int G, int MODE, bool ODD, bool FM>
+__device__ __forceinline__ void gfeed(GState<K, G, MODE>& S, const TierParams& P, int d, int lane,
+                                      unsigned gmask_) {
+    const unsigned gmask = FM ? 0xFFFFFFFFu : gmask_;
     using St = GState<K, G, MODE>;
     constexpr int SS = St::S;
-    const int d = S.d;
-    const int k0 = lane * SS;
-    int s_lo = ODD ? min(S.ls1 - 1, S.ls2) : min(S.ls1, S.ls2);
-    int s_hi = ODD ? max(S.hs1, S.hs2) : max(S.hs1 + 1, S.hs2);
-    const int fd = d >> 1;
-    int A = fd - S.ubase;
-    const int w = min(s_hi, A - max(d - S.m, 0)) - max(s_lo, A - min(d, S.n)) + 1;
-    uint32_t vml = gbits(0, SS - 1);                // this lane's in-matrix slots
-    uint32_t vmsl = gbits(0, 2 * SS - 1) & 0xAAAAAAAAu;
-    // group-uniform rare path
-    if ((s_lo < 0 || unsigned(s_hi) > unsigned(K - 1) || w > P.band || d >= S.d_lim) && !S.stop) {
-        if (s_hi < 0 || d > S.n + S.m + 1 || d > S.dcap) {
-            S.stop = kDone;
-        } else if (w > P.band) {
-            S.stop = kBand;
-            S.spread = w;
-        } else {
-            if (s_lo < 0 || s_hi > K - 1) {
-                const int wu = s_hi - s_lo + 1;
-                if (wu > K) {
-                    S.stop = kEscalate;
-                } else {
-                    const int sh = s_lo - ((K - wu) >> 1);
-                    for (int q = sh; q > 0; --q) {
-                        g_shift1<SS, G>(cur, 1, lane, gmask);
-                        g_shift1<SS, G>(prv, 1, lane, gmask);
-                    }
-                    for (int q = sh; q < 0; ++q) {
-                        g_shift1<SS, G>(cur, -1, lane, gmask);
-                        g_shift1<SS, G>(prv, -1, lane, gmask);
-                    }
-                    S.ubase += sh;
-                    S.ls1 -= sh;
-                    S.hs1 -= sh;
-                    S.ls2 -= sh;
-                    S.hs2 -= sh;
-                    A -= sh;
-                    g_limits(S);
-                    const int to_refill = 16 - int(it & 15);
-                    g_windows(S, P.pool, lane, ODD ? to_refill : to_refill - 1, to_refill);
-                }
-            }
-            if (d >= S.d_vm) {
-                const int klo = A - S.n;
-                const int khi = S.m - (d - fd) - S.ubase;
-                const int l = max(klo - k0, 0), h = min(min(khi, K - 1) - k0, SS - 1);
-                vml = gbits(l, h);
-                vmsl = (l > h) ? 0u : (gbits(2 * l, 2 * h + 1) & 0xAAAAAAAAu);
-            }
-        }
-    }
-    if (!S.stop) {
-        S.cells += max(w, 0);
-        S.delta_w = max(S.delta_w, w);
-    }
-
-    // gap source across the lane edge
-    int32_t edge;
-    if constexpr (ODD) {
-        edge = __shfl_down_sync(gmask, prv[0], 1, G);
-        if (lane == G - 1) edge = kDeadS;
-    } else {
-        edge = __shfl_up_sync(gmask, prv[SS - 1], 1, G);
-        if (lane == 0) edge = kDeadS;
-    }
-    [[maybe_unused]] uint32_t Z = 0;
-    if constexpr (MODE == 0) {
-        const uint32_t x = S.VW ^ S.HW;
-        Z = ~(x | (x << 1)) & vmsl;
-    }
-
-    const int32_t beta = -gap;
-    const int32_t negC = -((X << 6) + 63);
-    const int32_t c_init = (S.T + beta * d + 1) << 6;
-    // pass 1: candidates and keys (key' = 64 cand + s, lane-relative)
-    int32_t cand[SS], key[SS];
-#pragma unroll
-    for (int s = SS - 1; s >= 0; --s) {
-        const int32_t dg = cur[s];
-        int32_t db;
-        if constexpr (MODE == 0) {
-            const uint32_t t = (3u << (2 * s)) & (Z | P.pat);
-            db = s == 0 ? dg + int32_t(t) : dg + int32_t(__umulhi(t, 1u << (32 - 2 * s)));
-        } else {
-            const int r = s >> 2, q = s & 3;
-            uint32_t idx = 0;
-            switch (q) {  // bytes: v code, h code, 0, 0
-                case 0: asm("prmt.b32 %0, %1, %2, 0x8840;" : "=r"(idx) : "r"(S.VWb[r]), "r"(S.HWb[r])); break;
-                case 1: asm("prmt.b32 %0, %1, %2, 0x9951;" : "=r"(idx) : "r"(S.VWb[r]), "r"(S.HWb[r])); break;
-                case 2: asm("prmt.b32 %0, %1, %2, 0xAA62;" : "=r"(idx) : "r"(S.VWb[r]), "r"(S.HWb[r])); break;
-                default: asm("prmt.b32 %0, %1, %2, 0xBB73;" : "=r"(idx) : "r"(S.VWb[r]), "r"(S.HWb[r])); break;
-            }
-            db = dg + int32_t(tab[idx]);
-        }
-        int32_t ln, un;
-        if constexpr (ODD) {  // gap sources at u and u+1
-            ln = prv[s];
-            un = s < SS - 1 ? prv[s < SS - 1 ? s + 1 : s] : edge;
-        } else {              // gap sources at u-1 and u
-            ln = s > 0 ? prv[s > 0 ? s - 1 : s] : edge;
-            un = prv[s];
-        }
-        cand[s] = __vimax3_s32(db, ln, un);
-        key[s] = cand[s] * 64 + s;
-    }
-    // pass 2: exclusive suffix maximum of (key - C) over the higher lanes
-    int32_t M = key[0];
-#pragma unroll
-    for (int s = 1; s < SS; ++s) M = max(M, key[s]);
-    M += k0;  // true keys carry the global slot index
-#pragma unroll
-    for (int o = 1; o < G; o <<= 1) {
-        const int32_t y = __shfl_down_sync(gmask, M, o, G);
-        if (lane + o < G) M = max(M, y);
-    }
-    int32_t above = __shfl_down_sync(gmask, M, 1, G);
-    int32_t c = lane == G - 1 ? c_init : __viaddmax_s32(above, negC, c_init);
-    // pass 3: lane-local chain, drop test, dead mask (lane-relative keys)
-    c -= k0;
-    uint32_t dm = 0u;
-#pragma unroll
-    for (int s = SS - 1; s >= 0; --s) {
-        c = __viaddmax_s32(key[s], negC, c);
-        if (key[s] < c) {
-            cand[s] = kDeadS;
-            dm |= 1u << s;
-        }
-        cur[s] = cand[s];
-    }
-    c += k0;
-    // lane 0 ends the chain: the antidiagonal's best
-    const int32_t cf = __shfl_sync(gmask, c, 0, G) + ((X << 6) + 63);
-    {
-        const int32_t qnew = cf >> 6;
-        const int32_t qold = S.T + beta * d + X + 1;
-        if (qnew > qold && !S.stop) {
-            S.T = qnew - beta * d - X - 1;
-            S.best_d = d;
-            S.best_i = A - (cf & 63);
-        }
-    }
-    // live slots of the group: OR-butterfly of lane masks
-    {
-        const uint32_t lv = ~dm & vml;
-        int hs, ls;
-        bool any;
-        if constexpr (St::NM == 1) {
-            uint32_t full = lv << k0;
-#pragma unroll
-            for (int o = 1; o < G; o <<= 1) full |= __shfl_xor_sync(gmask, full, o, G);
-            any = full != 0u;
-            hs = 31 - __clz(full);
-            ls = __ffs(full) - 1;
-        } else {
-            uint64_t full = uint64_t(lv) << k0;
-#pragma unroll
-            for (int o = 1; o < G; o <<= 1) full |= __shfl_xor_sync(gmask, full, o, G);
-            any = full != 0ull;
-            hs = 63 - __clzll((long long)full);
-            ls = __ffsll((long long)full) - 1;
-        }
-        S.ls2 = S.ls1;
-        S.hs2 = S.hs1;
-        S.ls1 = any ? ls : kBig;
-        S.hs1 = any ? hs : -kBig;
-    }
-    // symbols entering on d+1
     if constexpr (MODE == 0) {
         if constexpr (ODD) {  // v: slot k <- k-1, new symbol at slot 0 (lane 0's reader)
             const uint32_t out = (S.VW >> (2 * (SS - 1))) & 3u;
@@ -298,6 +161,7 @@ __device__ __forceinline__ void gstep(GState<K, G, MODE>& S, int32_t (&cur)[K / 
         constexpr int ENC = MODE == 1 ? ENC_2BIT : ENC_5BIT;
         constexpr int NB = St::NB;
         constexpr int top = 8 * ((SS - 1) & 3);  // bit offset of slot SS-1 in its word
+        const int fd = d >> 1;
         if constexpr (ODD) {
             const uint32_t out = (S.VWb[NB - 1] >> top) & 0xFFu;
             uint32_t in = __shfl_up_sync(gmask, out, 1, G);
@@ -316,6 +180,277 @@ __device__ __forceinline__ void gstep(GState<K, G, MODE>& S, int32_t (&cur)[K / 
             S.HWb[NB - 1] = ((S.HWb[NB - 1] >> 8) & (keep >> 8)) | (in << top);
         }
     }
+}
+
+// Records the outcome of the group's unit at the deciding step (see the
+// thread tier's finish_unit); escalations save a resume record, each lane
+// writing its own slots.
+template <int K, int G, int MODE>
+__device__ __forceinline__ void gfinish(GState<K, G, MODE>& S, const TierParams& P, int code, int spread,
+                                        GSink& sk, int32_t beta, const int32_t (&cur)[K / G],
+                                        const int32_t (&prv)[K / G], int lane, unsigned gmask) {
+    constexpr int SS = K / G;
+    constexpr int KB = GState<K, G, MODE>::KB;
+    S.stop = code;
+    if (P.pilot) {
+        if (lane == 0) P.pilot_w[sk.qidx] = code == kEscalate ? -1 : S.delta_w;
+        return;
+    }
+    if (code == kEscalate) {
+        uint32_t entry = uint32_t(S.unit);
+        if (sk.resumable) {
+            unsigned long long r = 0;
+            if (lane == 0) r = atomicAdd(&P.ctr->resume_next, 1ull);
+            r = __shfl_sync(gmask, r, 0, G);
+            if (r < (unsigned long long)kResumeCap) {
+                int32_t* rec = P.resume + (long long)r * kResumeStride;
+#pragma unroll
+                for (int s = 0; s < SS; ++s) {
+                    rec[kRecRows + lane * SS + s] = cur[s];
+                    rec[kRecRows + K + lane * SS + s] = prv[s];
+                }
+                if (lane == 0) {
+                    rec[kRecUnit] = S.unit;
+                    rec[kRecD] = S.d;
+                    rec[kRecUbase] = S.ubase;
+                    rec[kRecTc] = S.Tc - (beta << 6);  // as before step d
+                    rec[kRecBestD] = S.best_d;
+                    rec[kRecBestU] = S.best_u;
+                    rec[kRecCells] = S.cells;
+                    rec[kRecDeltaW] = S.delta_w;
+                    rec[kRecHs1] = S.hs1;
+                    rec[kRecLs1] = S.hs1 < 0 ? -1 : KB - S.lr1;
+                    rec[kRecHs2] = S.hs2;
+                    rec[kRecLs2] = S.hs2 < 0 ? -1 : KB - S.lr2;
+                    rec[kRecK] = K;
+                }
+                entry = kResumeFlag | uint32_t(r);
+            }
+        }
+        if (lane == 0) {
+            const unsigned long long slot = atomicAdd(sk.esc_len, 1ull);
+            sk.esc_list[slot] = entry;
+            ++sk.esc;
+        }
+        return;
+    }
+    if (lane != 0) return;
+    DevResult res;
+    res.cells = S.cells;
+    res.delta_w = S.delta_w;
+    if (code == kBand) {
+        res.score = res.h_ext = res.v_ext = 0;
+        res.status = kStatusBand;
+        res.spread = spread;
+    } else {
+        const int best_i = (S.best_d >> 1) - S.best_u;
+        res.score = (S.Tc >> 6) - beta * S.d - 1;
+        res.h_ext = S.best_d - best_i;
+        res.v_ext = best_i;
+        res.status = kStatusOk;
+        res.spread = 0;
+    }
+    P.results[S.unit] = res;
+    ++sk.units;
+    sk.cells += (unsigned long long)S.cells;
+}
+
+template <int K, int G, int MODE, bool ODD, bool FM>
+__device__ __forceinline__ void gstep(GState<K, G, MODE>& S, int32_t (&cur)[K / G],
+                                      int32_t (&prv)[K / G], const TierParams& P,
+                                      const int8_t* __restrict__ tab, int32_t gap, int32_t X,
+                                      unsigned it, int lane, unsigned gmask, GSink& sk) {
+    // the main-path shuffles use the full mask when the whole warp steps
+    // together; the rare path (group-divergent) always uses the group's mask
+    const unsigned smask = FM ? 0xFFFFFFFFu : gmask;
+    using St = GState<K, G, MODE>;
+    constexpr int SS = St::S;
+    constexpr int KB = St::KB;
+    const int d = S.d;
+    const int k0 = lane * SS;
+    const int32_t beta = -gap;
+    S.Tc += beta << 6;
+    // window of row d, unclamped below d_vm (see the thread tier's xstep)
+    const int M = ODD ? max(S.lr1 + 1, S.lr2) : max(S.lr1, S.lr2);  // KB - s_lo
+    const int s_hi = ODD ? max(S.hs1, S.hs2) : max(S.hs1 + 1, S.hs2);
+    int wm1 = s_hi + M - KB;
+    uint32_t vml = gbits(0, SS - 1);  // this lane's in-matrix slots
+    [[maybe_unused]] uint32_t inv = 0u;
+    // group-uniform rare path
+    if ((M > KB || unsigned(s_hi) > unsigned(K - 1) || unsigned(wm1) >= unsigned(P.band) ||
+         d >= S.d_lim) && !S.stop) {
+        const bool e1 = S.hs1 < 0, e2 = S.hs2 < 0;
+        if ((e1 && e2) || d > S.n + S.m + 1 || d > S.dcap) {
+            gfinish<K, G, MODE>(S, P, kDone, 0, sk, beta, cur, prv, lane, gmask);
+        } else {
+            int lo = kBig, hi = -kBig;
+            if (!e1) {
+                lo = KB - S.lr1 - (ODD ? 1 : 0);
+                hi = S.hs1 + (ODD ? 0 : 1);
+            }
+            if (!e2) {
+                lo = min(lo, KB - S.lr2);
+                hi = max(hi, S.hs2);
+            }
+            const int fd = d >> 1;
+            int A = fd - S.ubase;
+            const int w = min(hi, A - max(d - S.m, 0)) - max(lo, A - min(d, S.n)) + 1;
+            if (w > P.band) {
+                gfinish<K, G, MODE>(S, P, kBand, w, sk, beta, cur, prv, lane, gmask);
+            } else {
+                if (lo < 0 || hi > K - 1) {
+                    const int wu = hi - lo + 1;
+                    if (wu > K) {
+                        gfinish<K, G, MODE>(S, P, kEscalate, 0, sk, beta, cur, prv, lane, gmask);
+                    } else {
+                        const int sh = lo - ((K - wu) >> 1);
+                        for (int q = sh; q > 0; --q) {
+                            g_shift1<SS, G>(cur, 1, lane, gmask);
+                            g_shift1<SS, G>(prv, 1, lane, gmask);
+                        }
+                        for (int q = sh; q < 0; ++q) {
+                            g_shift1<SS, G>(cur, -1, lane, gmask);
+                            g_shift1<SS, G>(prv, -1, lane, gmask);
+                        }
+                        S.ubase += sh;
+                        if (!e1) {
+                            S.hs1 -= sh;
+                            S.lr1 += sh;
+                        }
+                        if (!e2) {
+                            S.hs2 -= sh;
+                            S.lr2 += sh;
+                        }
+                        A -= sh;
+                        g_limits(S);
+                        const int to_refill = 16 - int(it & 15);
+                        g_windows(S, P.pool, lane, ODD ? to_refill : to_refill - 1, to_refill);
+                    }
+                }
+                if (!S.stop && d >= S.d_vm) {
+                    const int klo = A - S.n;
+                    const int khi = S.m - (d - fd) - S.ubase;
+                    const int l = max(klo - k0, 0), h = min(min(khi, K - 1) - k0, SS - 1);
+                    vml = gbits(l, h);
+                    inv = ~((l > h) ? 0u : gbits(2 * l, 2 * h + 1));
+                }
+                wm1 = max(w, 0) - 1;
+            }
+        }
+    }
+    S.cells += wm1 + 1;
+    S.delta_w = max(S.delta_w, wm1 + 1);
+
+    // gap source across the lane edge
+    int32_t edge;
+    if constexpr (ODD) {
+        edge = __shfl_down_sync(smask, prv[0], 1, G);
+        if (lane == G - 1) edge = kDeadS;
+    } else {
+        edge = __shfl_up_sync(smask, prv[SS - 1], 1, G);
+        if (lane == 0) edge = kDeadS;
+    }
+    // match bytes (see the thread tier): byte j of Z[q] = 1 + 2*match of slot 4j+q
+    [[maybe_unused]] uint32_t Z[4];
+    if constexpr (MODE == 0) {
+        const uint32_t x = glop3<0xBE>(S.VW, S.HW, inv);  // (a ^ b) | c
+        const uint32_t z = ~(x | (x << 1));
+#pragma unroll
+        for (int q = 0; q < 4; ++q) Z[q] = ((z >> (2 * q)) & 0x02020202u) | 0x01010101u;
+    }
+
+    const int32_t negC = -((X << 6) + 63);
+    // pass 1: candidates and keys (key' = 64 cand + s, lane-relative)
+    int32_t cand[SS], key[SS];
+#pragma unroll
+    for (int s = SS - 1; s >= 0; --s) {
+        const int32_t dg = cur[s];
+        int32_t db;
+        if constexpr (MODE == 0) {
+            db = __dp4a(int(Z[s & 3]), 1 << (8 * ((s >> 2) & 3)), dg);
+        } else {
+            const int r = s >> 2, q = s & 3;
+            uint32_t idx = 0;
+            switch (q) {  // bytes: v code, h code, 0, 0
+                case 0: asm("prmt.b32 %0, %1, %2, 0x8840;" : "=r"(idx) : "r"(S.VWb[r]), "r"(S.HWb[r])); break;
+                case 1: asm("prmt.b32 %0, %1, %2, 0x9951;" : "=r"(idx) : "r"(S.VWb[r]), "r"(S.HWb[r])); break;
+                case 2: asm("prmt.b32 %0, %1, %2, 0xAA62;" : "=r"(idx) : "r"(S.VWb[r]), "r"(S.HWb[r])); break;
+                default: asm("prmt.b32 %0, %1, %2, 0xBB73;" : "=r"(idx) : "r"(S.VWb[r]), "r"(S.HWb[r])); break;
+            }
+            db = dg + int32_t(tab[idx]);
+        }
+        int32_t ln, un;
+        if constexpr (ODD) {  // gap sources at u and u+1
+            ln = prv[s];
+            un = s < SS - 1 ? prv[s < SS - 1 ? s + 1 : s] : edge;
+        } else {              // gap sources at u-1 and u
+            ln = s > 0 ? prv[s > 0 ? s - 1 : s] : edge;
+            un = prv[s];
+        }
+        cand[s] = __vimax3_s32(db, ln, un);
+        key[s] = cand[s] * 64 + s;
+    }
+    // pass 2: one all-gather round of the lane maxima gives every lane the
+    // maximum over the higher lanes (its chain input) and the group maximum
+    // (the chain's end, i.e. the antidiagonal's running best)
+    int32_t Mk = key[0];
+#pragma unroll
+    for (int s = 1; s < SS; ++s) Mk = max(Mk, key[s]);
+    Mk += k0;  // true keys carry the group slot index
+    int32_t above = -(1 << 30), all = -(1 << 30);  // below every key, and -C cannot wrap
+    {
+        int32_t Mj[G];
+#pragma unroll
+        for (int j = 0; j < G; ++j) Mj[j] = __shfl_sync(smask, Mk, j, G);
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+            all = max(all, Mj[j]);
+            if (j > lane) above = max(above, Mj[j]);
+        }
+    }
+    int32_t c = __viaddmax_s32(above, negC, S.Tc);
+    // pass 3: lane-local chain, drop test, dead mask (lane-relative keys)
+    c -= k0;
+    uint32_t dm = 0u;
+#pragma unroll
+    for (int s = SS - 1; s >= 0; --s) {
+        c = __viaddmax_s32(key[s], negC, c);
+        if (key[s] < c) {
+            cand[s] = kDeadS;
+            dm |= 1u << s;
+        }
+        cur[s] = cand[s];
+    }
+    // the chain's end: max(Tc, group max key - C)
+    const int32_t cf = __viaddmax_s32(all, negC, S.Tc);
+    if (cf != S.Tc) {
+        const int32_t c63 = cf + 63;
+        S.Tc = c63 & ~63;
+        S.best_d = d;
+        S.best_u = S.ubase + (c63 & 63);
+    }
+    // live slots of the group: one all-gather round of the lane masks
+    S.hs2 = S.hs1;
+    S.lr2 = S.lr1;
+    {
+        const uint32_t lv = ~dm & vml;
+        if constexpr (St::NM == 1) {
+            const uint32_t mine = lv << k0;
+            uint32_t full = 0u;
+#pragma unroll
+            for (int j = 0; j < G; ++j) full |= __shfl_sync(smask, mine, j, G);
+            S.hs1 = gbfind32(full);
+            S.lr1 = gbfind32(__brev(full));
+        } else {
+            const uint64_t mine = uint64_t(lv) << k0;
+            uint64_t full = 0ull;
+#pragma unroll
+            for (int j = 0; j < G; ++j) full |= __shfl_sync(smask, mine, j, G);
+            S.hs1 = gbfind64(full);
+            S.lr1 = gbfind64(__brevll(full));
+        }
+    }
+    gfeed<K, G, MODE, ODD, FM>(S, P, d, lane, gmask);
     S.d = d + 1;
 }
 
@@ -323,12 +458,14 @@ template <int K, int G, int MODE>
 __global__ void __launch_bounds__(128) group_tier_kernel(TierParams P) {
     using St = GState<K, G, MODE>;
     constexpr int SS = St::S;
+    constexpr int KB = St::KB;
     __shared__ int8_t tab[MODE == 0 ? 4 : 32 * 256];
     const int32_t gap = P.scheme->gap, X = P.scheme->x;
     const int wl = threadIdx.x & 31;
     const int lane = wl % G;
     const int gbase = wl - lane;
     const unsigned gmask = (G == 32 ? 0xFFFFFFFFu : ((1u << G) - 1u)) << gbase;
+    const int k0 = lane * SS;
 
     Queue Q;
     if (!make_queue(P, Q)) return;
@@ -345,14 +482,27 @@ __global__ void __launch_bounds__(128) group_tier_kernel(TierParams P) {
         __syncthreads();
     }
     const int next_tier = P.esc_to_warp ? kWarpTier : P.tier + 1;
-    uint32_t* esc_list = P.lists + (long long)next_tier * P.n_units;
-    unsigned long long* esc_len = &P.ctr->list_len[next_tier];
-    unsigned long long my_units = 0, my_cells = 0, my_esc = 0;
+    GSink sk;
+    sk.esc_list = P.lists + (long long)next_tier * P.n_units;
+    sk.esc_len = &P.ctr->list_len[next_tier];
+    sk.qidx = 0;
+    sk.units = sk.cells = sk.esc = 0;
+    sk.resumable = next_tier != kWarpTier && !P.pilot;
 
+    // Every group of the warp executes every step, so the main-path shuffles
+    // can use the full mask; a group without a unit steps on harmless state
+    // with stop set (no rare path, no output, no loads: its reader refills
+    // are skipped and table-mode lookups see empty views).
     St S;
+    S.m = S.n = 0;
+    S.stop = kDone;
+    S.VW = S.HW = 0u;
+#pragma unroll
+    for (int r = 0; r < St::NB; ++r) S.VWb[r] = S.HWb[r] = 0u;
     int32_t E[SS], O[SS];
+#pragma unroll
+    for (int s = 0; s < SS; ++s) E[s] = O[s] = kDeadS;
     bool active = false;
-    long long qidx = 0;
     unsigned it = 0xFFFFFFFFu;
     auto fetch = [&]() {
         active = false;
@@ -360,14 +510,24 @@ __global__ void __launch_bounds__(128) group_tier_kernel(TierParams P) {
             unsigned long long i = 0;
             if (lane == 0) i = atomicAdd(Q.cursor, 1ull);
             i = __shfl_sync(gmask, i, 0, G);
-            if (i >= Q.len) return;
-            const uint32_t unit = Q.q[(long long)i * Q.stride];
+            if (i >= Q.len) {
+                S.stop = kDone;
+                S.m = S.n = 0;
+                return;
+            }
+            const uint32_t e = Q.q[(long long)i * Q.stride];
+            uint32_t unit = e;
+            const int32_t* rec = nullptr;
+            if (e & kResumeFlag) {
+                rec = P.resume + (long long)(e & ~kResumeFlag) * kResumeStride;
+                unit = uint32_t(rec[kRecUnit]);
+            }
             const DevUnit u = P.units[unit];
             if (u.route != 0) {
                 if (P.pilot && lane == 0) P.pilot_w[i] = -2;
                 continue;
             }
-            qidx = (long long)i;
+            sk.qidx = (long long)i;
             S.unit = int32_t(unit);
             S.h_pos = u.h_pos;
             S.v_pos = u.v_pos;
@@ -375,25 +535,57 @@ __global__ void __launch_bounds__(128) group_tier_kernel(TierParams P) {
             S.n = u.v_len;
             S.hdir = u.dir & 1;
             S.vdir = (u.dir >> 1) & 1;
-            S.d = 1;
             S.dcap = P.pilot ? P.pilot_cap : (INT_MAX >> 1);
-            S.ubase = -(K / 2);
-            S.ls1 = S.hs1 = K / 2;
-            S.ls2 = kBig;
-            S.hs2 = -kBig;
             S.stop = 0;
-            S.spread = 0;
-            S.T = S.best_d = S.best_i = 0;
-            S.delta_w = 1;
-            S.cells = 1;
-            g_limits(S);
-#pragma unroll
-            for (int s = 0; s < SS; ++s) {
-                O[s] = kDeadS;
-                E[s] = (lane * SS + s == K / 2) ? X + 1 : kDeadS;
-            }
             const int r = 15 - int(it & 15);
-            g_windows(S, P.pool, lane, r, r);
+            if (!rec) {
+                S.d = 1;
+                S.ubase = -(K / 2);
+                S.hs1 = K / 2;
+                S.lr1 = KB - K / 2;
+                S.hs2 = S.lr2 = -1;
+                S.Tc = 64;
+                S.best_d = S.best_u = 0;
+                S.delta_w = 1;
+                S.cells = 1;
+#pragma unroll
+                for (int s = 0; s < SS; ++s) {
+                    O[s] = kDeadS;
+                    E[s] = (k0 + s == K / 2) ? X + 1 : kDeadS;
+                }
+                g_limits(S);
+                g_windows(S, P.pool, lane, r, r);
+            } else {
+                // continue from a narrower tier's record (see resume_unit)
+                const int ko = rec[kRecK];
+                const int off = (K - ko) >> 1;
+                const int d = rec[kRecD];
+                S.ubase = rec[kRecUbase] - off;
+                S.Tc = rec[kRecTc];
+                S.best_d = rec[kRecBestD];
+                S.best_u = rec[kRecBestU];
+                S.cells = rec[kRecCells];
+                S.delta_w = rec[kRecDeltaW];
+                const int h1 = rec[kRecHs1], l1 = rec[kRecLs1], h2 = rec[kRecHs2], l2 = rec[kRecLs2];
+                S.hs1 = h1 < 0 ? -1 : h1 + off;
+                S.lr1 = h1 < 0 ? -1 : KB - (l1 + off);
+                S.hs2 = h2 < 0 ? -1 : h2 + off;
+                S.lr2 = h2 < 0 ? -1 : KB - (l2 + off);
+                const bool odd = d & 1;
+#pragma unroll
+                for (int s = 0; s < SS; ++s) {
+                    const int src = k0 + s - off;
+                    const bool in = src >= 0 && src < ko;
+                    const int32_t vc = in ? rec[kRecRows + src] : kDeadS;
+                    const int32_t vp = in ? rec[kRecRows + ko + src] : kDeadS;
+                    O[s] = odd ? vc : vp;
+                    E[s] = odd ? vp : vc;
+                }
+                S.d = odd ? d : d - 1;
+                g_windows(S, P.pool, lane, r, r);
+                S.d = d;
+                g_limits(S);
+            }
             active = true;
             return;
         }
@@ -401,53 +593,29 @@ __global__ void __launch_bounds__(128) group_tier_kernel(TierParams P) {
     fetch();
     it = 0;
     while (__any_sync(0xFFFFFFFFu, active)) {
-        if (active) {
-            if constexpr (MODE == 0) {
-                if ((it & 15) == 0) {
-                    if (lane == 0) S.rv.refill(P.pool);
-                    if (lane == G - 1) S.rh.refill(P.pool);
-                }
-            }
-            gstep<K, G, MODE, true>(S, O, E, P, tab, gap, X, it, lane, gmask);
-            gstep<K, G, MODE, false>(S, E, O, P, tab, gap, X, it, lane, gmask);
-            if (S.stop) {
-                const int r = S.stop;
-                if (lane == 0) {
-                    if (P.pilot) {
-                        P.pilot_w[qidx] = r == kEscalate ? -1 : S.delta_w;
-                    } else if (r == kEscalate) {
-                        const unsigned long long slot = atomicAdd(esc_len, 1ull);
-                        esc_list[slot] = uint32_t(S.unit);
-                        ++my_esc;
-                    } else {
-                        DevResult res;
-                        res.cells = S.cells;
-                        res.delta_w = S.delta_w;
-                        if (r == kBand) {
-                            res.score = res.h_ext = res.v_ext = 0;
-                            res.status = kStatusBand;
-                            res.spread = S.spread;
-                        } else {
-                            res.score = S.T;
-                            res.h_ext = S.best_d - S.best_i;
-                            res.v_ext = S.best_i;
-                            res.status = kStatusOk;
-                            res.spread = 0;
-                        }
-                        P.results[S.unit] = res;
-                        ++my_units;
-                        my_cells += (unsigned long long)S.cells;
-                    }
-                }
-                fetch();
+        if constexpr (MODE == 0) {
+            if (active && (it & 15) == 0) {
+                if (lane == 0) S.rv.refill(P.pool);
+                if (lane == G - 1) S.rh.refill(P.pool);
             }
         }
+        const bool peel = active && !(S.d & 1);
+        if (__any_sync(0xFFFFFFFFu, peel)) {  // rare: some group resumed at an even d
+            if (peel)  // its odd half only feeds v
+                gfeed<K, G, MODE, true, false>(S, P, S.d - 1, lane, gmask);
+            else
+                gstep<K, G, MODE, true, false>(S, O, E, P, tab, gap, X, it, lane, gmask, sk);
+        } else {
+            gstep<K, G, MODE, true, true>(S, O, E, P, tab, gap, X, it, lane, gmask, sk);
+        }
+        gstep<K, G, MODE, false, true>(S, E, O, P, tab, gap, X, it, lane, gmask, sk);
+        if (active && S.stop) fetch();  // outcome already recorded by the deciding step
         ++it;
     }
     if (P.pilot || lane != 0) return;
-    if (my_units) atomicAdd(&P.ctr->units[P.tier], my_units);
-    if (my_cells) atomicAdd(&P.ctr->cells[P.tier], my_cells);
-    if (my_esc) atomicAdd(&P.ctr->escalated[P.tier], my_esc);
+    if (sk.units) atomicAdd(&P.ctr->units[P.tier], sk.units);
+    if (sk.cells) atomicAdd(&P.ctr->cells[P.tier], sk.cells);
+    if (sk.esc) atomicAdd(&P.ctr->escalated[P.tier], sk.esc);
 }
 
 #define XB_GINST(K, G)                                                     \

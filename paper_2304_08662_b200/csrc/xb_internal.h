@@ -57,6 +57,20 @@ struct DevCounters {
     unsigned long long dbg[8];         // XB_COUNTERS builds: steps, rare, masked, recenters, stops
     int32_t start_tier;                // chosen by the pilot
     int32_t pad;
+    unsigned long long resume_next;    // resume records handed out
+};
+
+// Resume records: a unit that outgrows its tier saves its band state at the
+// antidiagonal that did not fit, and the wider tier continues from there
+// instead of re-running it.  An escalation-list entry with kResumeFlag set
+// indexes a record; a plain entry is a unit to start from scratch (records
+// exhausted, or the next tier is the warp tier).
+constexpr int kResumeCap = 32768;
+constexpr int kResumeStride = 128;  // int32 per record: 16 header + 2 * K_old row values
+constexpr uint32_t kResumeFlag = 0x80000000u;
+enum : int {
+    kRecUnit = 0, kRecD, kRecUbase, kRecTc, kRecBestD, kRecBestU, kRecCells, kRecDeltaW,
+    kRecHs1, kRecLs1, kRecHs2, kRecLs2, kRecK, kRecRows = 16
 };
 
 constexpr int kStatusOk = 0;

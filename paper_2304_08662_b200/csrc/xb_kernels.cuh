@@ -62,6 +62,7 @@ struct TierParams {
     int32_t esc_to_warp;                 // escalations skip the wider thread tiers
     int32_t role;                        // kRole*: which of the tier's queues this launch serves
     int32_t* __restrict__ warp_scratch;  // warp tier: 2*band ints per warp slot
+    int32_t* __restrict__ resume;        // kResumeCap records of kResumeStride ints
     // opaque constants: kept in c[]/uniform registers so ptxas cannot fold
     // them into ALU-pipe forms (LEA, LOP3 immediates, SEL)
     uint32_t pat;                        // 0x55555555

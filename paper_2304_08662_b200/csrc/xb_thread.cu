@@ -124,6 +124,46 @@ __device__ __forceinline__ void start_unit(TState<K, MODE>& S, int32_t (&E)[K], 
     init_windows(S, P.pool, r, r);
 }
 
+// Continues a unit from a resume record written by a narrower tier: the
+// saved band is centred in this one, and the windows are rebuilt at d (at
+// d-1 when d is even: that iteration only feeds the v symbol, see the loop).
+template <int K, int MODE>
+__device__ __forceinline__ void resume_unit(TState<K, MODE>& S, int32_t (&E)[K], int32_t (&O)[K],
+                                            const TierParams& P, const int32_t* __restrict__ rec,
+                                            unsigned it) {
+    constexpr int KB = 32 * TState<K, MODE>::NM - 1;
+    const int ko = rec[kRecK];
+    const int off = (K - ko) >> 1;
+    const int d = rec[kRecD];
+    S.d = d;
+    S.ubase = rec[kRecUbase] - off;
+    S.Tc = rec[kRecTc];
+    S.best_d = rec[kRecBestD];
+    S.best_u = rec[kRecBestU];
+    S.cells = rec[kRecCells];
+    S.delta_w = rec[kRecDeltaW];
+    const int h1 = rec[kRecHs1], l1 = rec[kRecLs1], h2 = rec[kRecHs2], l2 = rec[kRecLs2];
+    S.hs1 = h1 < 0 ? -1 : h1 + off;
+    S.lr1 = h1 < 0 ? -1 : KB - (l1 + off);
+    S.hs2 = h2 < 0 ? -1 : h2 + off;
+    S.lr2 = h2 < 0 ? -1 : KB - (l2 + off);
+    set_limits(S);
+    const bool odd = d & 1;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const int src = k - off;
+        const bool in = src >= 0 && src < ko;
+        const int32_t vc = in ? rec[kRecRows + src] : kDeadS;       // row d-2
+        const int32_t vp = in ? rec[kRecRows + ko + src] : kDeadS;  // row d-1
+        O[k] = odd ? vc : vp;
+        E[k] = odd ? vp : vc;
+    }
+    const int r = 15 - int(it & 15);
+    S.d = odd ? d : d - 1;
+    init_windows(S, P.pool, r, r);
+    S.d = d;
+}
+
 // ---- one slot -------------------------------------------------------------
 
 struct SlotCtx {
@@ -217,6 +257,41 @@ __device__ __forceinline__ void all_slots(std::integer_sequence<int, ks...>, int
     (slot<K, MODE, ODD, K - 1 - ks>(cur, prv, Z, S, P, tab, X, dm), ...);
 }
 
+// Shifts the symbol windows for antidiagonal d+1 (the symbol entering the
+// band after step d: v on odd d, h on even d).
+template <int K, int MODE, bool ODD>
+__device__ __forceinline__ void feed(TState<K, MODE>& S, const TierParams& P, int d) {
+    using St = TState<K, MODE>;
+    if constexpr (ODD) {  // floor((d+1)/2) grows: v[a+1] enters at slot 0
+        if constexpr (MODE == 0) {
+#pragma unroll
+            for (int w = St::NW - 1; w > 0; --w) S.VW[w] = __funnelshift_l(S.VW[w - 1], S.VW[w], 2);
+            S.VW[0] = __funnelshift_l(S.rv.cur, S.VW[0], 2);
+            S.rv.cur <<= 2;
+        } else {
+            constexpr int ENC = MODE == 1 ? ENC_2BIT : ENC_5BIT;
+            const uint32_t code = code_at<ENC>(P.pool, S.v_pos, S.vdir, S.n, int64_t(d >> 1) - S.ubase);
+#pragma unroll
+            for (int r = St::NB - 1; r > 0; --r) S.VW[r] = __funnelshift_l(S.VW[r - 1], S.VW[r], 8);
+            S.VW[0] = (S.VW[0] << 8) | code;
+        }
+    } else {  // ceil((d+1)/2) grows: h[b+WK] enters at slot WK-1
+        if constexpr (MODE == 0) {
+#pragma unroll
+            for (int w = 0; w < St::NW - 1; ++w) S.HW[w] = __funnelshift_r(S.HW[w], S.HW[w + 1], 2);
+            S.HW[St::NW - 1] = __funnelshift_r(S.HW[St::NW - 1], S.rh.cur, 2);
+            S.rh.cur >>= 2;
+        } else {
+            constexpr int ENC = MODE == 1 ? ENC_2BIT : ENC_5BIT;
+            const uint32_t code =
+                code_at<ENC>(P.pool, S.h_pos, S.hdir, S.m, int64_t(d - (d >> 1)) + S.ubase - 1 + St::WK);
+#pragma unroll
+            for (int r = 0; r < St::NB - 1; ++r) S.HW[r] = __funnelshift_r(S.HW[r], S.HW[r + 1], 8);
+            S.HW[St::NB - 1] = __funnelshift_r(S.HW[St::NB - 1], code, 8);
+        }
+    }
+}
+
 // Where a finished unit's outcome goes: its result row, the next tier's
 // escalation list, or (pilot) the widest window seen.
 struct Sink {
@@ -224,21 +299,57 @@ struct Sink {
     unsigned long long* esc_len;
     long long qidx;
     unsigned long long units, cells, esc;
+    bool resumable;  // the next tier takes resume records (a thread or lane-group tier)
 };
+
+// Saves the band state of a unit that does not fit at antidiagonal d (the
+// step has changed nothing yet: cur = row d-2, prv = row d-1) and returns
+// the escalation-list entry: a record index, or the bare unit when the
+// records are used up.
+template <int K, int MODE>
+__device__ __forceinline__ uint32_t save_resume(const TState<K, MODE>& S, const int32_t (&cur)[K],
+                                                const int32_t (&prv)[K], const TierParams& P,
+                                                int32_t beta) {
+    constexpr int KB = 32 * TState<K, MODE>::NM - 1;
+    const unsigned long long r = atomicAdd(&P.ctr->resume_next, 1ull);
+    if (r >= (unsigned long long)kResumeCap) return uint32_t(S.unit);
+    int32_t* rec = P.resume + (long long)r * kResumeStride;
+    rec[kRecUnit] = S.unit;
+    rec[kRecD] = S.d;
+    rec[kRecUbase] = S.ubase;
+    rec[kRecTc] = S.Tc - (beta << 6);  // as before step d
+    rec[kRecBestD] = S.best_d;
+    rec[kRecBestU] = S.best_u;
+    rec[kRecCells] = S.cells;
+    rec[kRecDeltaW] = S.delta_w;
+    rec[kRecHs1] = S.hs1;
+    rec[kRecLs1] = S.hs1 < 0 ? -1 : KB - S.lr1;
+    rec[kRecHs2] = S.hs2;
+    rec[kRecLs2] = S.hs2 < 0 ? -1 : KB - S.lr2;
+    rec[kRecK] = K;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        rec[kRecRows + k] = cur[k];
+        rec[kRecRows + K + k] = prv[k];
+    }
+    return kResumeFlag | uint32_t(r);
+}
 
 // Records the outcome of the current unit at the step that decides it (the
 // rest of that loop iteration is dead work nobody reads) and sets S.stop.
 template <int K, int MODE>
 __device__ __forceinline__ void finish_unit(TState<K, MODE>& S, const TierParams& P, int code, int spread,
-                                         Sink& sk, int32_t beta) {
+                                            Sink& sk, int32_t beta, const int32_t (&cur)[K],
+                                            const int32_t (&prv)[K]) {
     S.stop = code;
     if (P.pilot) {
         P.pilot_w[sk.qidx] = code == kEscalate ? -1 : S.delta_w;
         return;
     }
     if (code == kEscalate) {
+        const uint32_t entry = sk.resumable ? save_resume(S, cur, prv, P, beta) : uint32_t(S.unit);
         const unsigned long long slot = atomicAdd(sk.esc_len, 1ull);
-        sk.esc_list[slot] = uint32_t(S.unit);
+        sk.esc_list[slot] = entry;
         ++sk.esc;
         return;
     }
@@ -319,7 +430,7 @@ __device__ __forceinline__ void xstep(TState<K, MODE>& S, int32_t (&cur)[K], int
         XB_COUNT(1);
         const bool e1 = S.hs1 < 0, e2 = S.hs2 < 0;
         if ((e1 && e2) || d > S.n + S.m + 1 || d > S.dcap) {
-            finish_unit(S, P, kDone, 0, sk, beta);  // align.cpp:61-66
+            finish_unit(S, P, kDone, 0, sk, beta, cur, prv);  // align.cpp:61-66
         } else {
             int lo = kBig, hi = -kBig;
             if (!e1) {
@@ -335,13 +446,13 @@ __device__ __forceinline__ void xstep(TState<K, MODE>& S, int32_t (&cur)[K], int
             // clamp to the matrix: i <= min(d, n)  and  i >= max(d - m, 0)
             const int w = min(hi, A - max(d - S.m, 0)) - max(lo, A - min(d, S.n)) + 1;
             if (w > P.band) {  // align.cpp:93-94: first overflow, cells so far
-                finish_unit(S, P, kBand, w, sk, beta);
+                finish_unit(S, P, kBand, w, sk, beta, cur, prv);
             } else {
                 if (lo < 0 || hi > K - 1) {
                     // every live source lies inside the unclamped window, so it must fit
                     const int wu = hi - lo + 1;
                     if (wu > K) {
-                        finish_unit(S, P, kEscalate, 0, sk, beta);
+                        finish_unit(S, P, kEscalate, 0, sk, beta, cur, prv);
                     } else {
                         XB_COUNT(3);
                         const int sh = lo - ((K - wu) >> 1);  // new slot 0 = old slot sh
@@ -438,35 +549,7 @@ __device__ __forceinline__ void xstep(TState<K, MODE>& S, int32_t (&cur)[K], int
         S.lr1 = bfind64(__brevll(lv));
     }
 
-    // feed the symbol that enters the band on d+1
-    if constexpr (ODD) {  // floor((d+1)/2) grows: v[a+1] enters at slot 0
-        if constexpr (MODE == 0) {
-#pragma unroll
-            for (int w = St::NW - 1; w > 0; --w) S.VW[w] = __funnelshift_l(S.VW[w - 1], S.VW[w], 2);
-            S.VW[0] = __funnelshift_l(S.rv.cur, S.VW[0], 2);
-            S.rv.cur <<= 2;
-        } else {
-            constexpr int ENC = MODE == 1 ? ENC_2BIT : ENC_5BIT;
-            const uint32_t code = code_at<ENC>(P.pool, S.v_pos, S.vdir, S.n, int64_t(d >> 1) - S.ubase);
-#pragma unroll
-            for (int r = St::NB - 1; r > 0; --r) S.VW[r] = __funnelshift_l(S.VW[r - 1], S.VW[r], 8);
-            S.VW[0] = (S.VW[0] << 8) | code;
-        }
-    } else {  // ceil((d+1)/2) grows: h[b+WK] enters at slot WK-1
-        if constexpr (MODE == 0) {
-#pragma unroll
-            for (int w = 0; w < St::NW - 1; ++w) S.HW[w] = __funnelshift_r(S.HW[w], S.HW[w + 1], 2);
-            S.HW[St::NW - 1] = __funnelshift_r(S.HW[St::NW - 1], S.rh.cur, 2);
-            S.rh.cur >>= 2;
-        } else {
-            constexpr int ENC = MODE == 1 ? ENC_2BIT : ENC_5BIT;
-            const uint32_t code =
-                code_at<ENC>(P.pool, S.h_pos, S.hdir, S.m, int64_t(d - (d >> 1)) + S.ubase - 1 + St::WK);
-#pragma unroll
-            for (int r = 0; r < St::NB - 1; ++r) S.HW[r] = __funnelshift_r(S.HW[r], S.HW[r + 1], 8);
-            S.HW[St::NB - 1] = __funnelshift_r(S.HW[St::NB - 1], code, 8);
-        }
-    }
+    feed<K, MODE, ODD>(S, P, d);
     S.d = d + 1;
 }
 
@@ -499,6 +582,7 @@ __global__ void __launch_bounds__(kTB, tier_min_blocks<K>()) thread_tier_kernel(
     sk.esc_len = &P.ctr->list_len[next_tier];
     sk.qidx = 0;
     sk.units = sk.cells = sk.esc = 0;
+    sk.resumable = next_tier != kWarpTier && !P.pilot;
 #if XB_COUNTERS
     unsigned long long xb_dbg[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #endif
@@ -511,14 +595,21 @@ __global__ void __launch_bounds__(kTB, tier_min_blocks<K>()) thread_tier_kernel(
     unsigned it = 0xFFFFFFFFu;
     auto fetch = [&]() {
         active = false;
-        uint32_t unit;
-        while (Q.next(unit, sk.qidx)) {
+        uint32_t e;
+        while (Q.next(e, sk.qidx)) {
+            uint32_t unit = e;
+            const int32_t* rec = nullptr;
+            if (e & kResumeFlag) {
+                rec = P.resume + (long long)(e & ~kResumeFlag) * kResumeStride;
+                unit = uint32_t(rec[kRecUnit]);
+            }
             // units whose values could leave the drift-space range go to the warp tier
             if (P.units[unit].route != 0) {
                 if (P.pilot) P.pilot_w[sk.qidx] = -2;  // not a thread-tier unit
                 continue;
             }
             start_unit<K, MODE>(S, E, O, P, unit, X, it);
+            if (rec) resume_unit<K, MODE>(S, E, O, P, rec, it);
             active = true;
             return;
         }
@@ -534,11 +625,19 @@ __global__ void __launch_bounds__(kTB, tier_min_blocks<K>()) thread_tier_kernel(
                     S.rh.refill(P.pool);
                 }
             }
+            // iterations start on odd d, except right after a resume at an even
+            // d, where the odd half only feeds its v symbol
 #if XB_COUNTERS
-            xstep<K, MODE, true>(S, O, E, P, tab, gap, X, it, sk, xb_dbg);
+            if (S.d & 1)
+                xstep<K, MODE, true>(S, O, E, P, tab, gap, X, it, sk, xb_dbg);
+            else
+                feed<K, MODE, true>(S, P, S.d - 1);
             xstep<K, MODE, false>(S, E, O, P, tab, gap, X, it, sk, xb_dbg);
 #else
-            xstep<K, MODE, true>(S, O, E, P, tab, gap, X, it, sk);
+            if (S.d & 1)
+                xstep<K, MODE, true>(S, O, E, P, tab, gap, X, it, sk);
+            else
+                feed<K, MODE, true>(S, P, S.d - 1);
             xstep<K, MODE, false>(S, E, O, P, tab, gap, X, it, sk);
 #endif
             if (S.stop) {  // outcome already recorded by the deciding step

@@ -1,11 +1,14 @@
 #!/bin/bash
-# parity + C5 timing + (NCU=1) one full ncu capture of the start-tier kernel
+# parity + timing (C5 by default; CONFIGS="1 2 3" etc.) + (NCU=1) one full ncu capture
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -5 > gpurun_out/q_tests.log
+timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -5 > gpurun_out/q_tests.log
 ok=1
-for f in 0 64; do
-  out=$(timeout 300 python scripts/prof_run.py --config 5 --scale ${SCALE:-0.2} --runs 3 --flags $f 2>&1) || ok=0
-  echo "flags $f: $(echo "$out" | tail -1)"
+for c in ${CONFIGS:-5}; do
+  sc=1.0; [ $c = 5 ] && sc=${SCALE:-0.2}; [ $c = 4 ] && sc=0.2
+  for f in ${FLAGS:-0 64}; do
+    out=$(timeout 300 python scripts/prof_run.py --config $c --scale $sc --runs 3 --flags $f 2>&1) || ok=0
+    echo "cfg $c flags $f: $(echo "$out" | tail -1 | sed 's/.*tiers ms/tiers ms/')"
+  done
 done > gpurun_out/q_prof.log 2>&1
 cat gpurun_out/q_tests.log gpurun_out/q_prof.log
 if [ -n "$NCU" ] && [ $ok = 1 ]; then

@@ -56,9 +56,10 @@ def _by_scheme(entries):
 
 # 64 = NO_GROUP (one thread per unit), 32 = GROUP (lane groups throughout),
 # 8 | t << 8 = start at tier t without the pilot
-TIER_FLAGS = ([0, 2, 64] + [64 | 8 | (t << 8) for t in range(5)]
+# 128 = THROUGHPUT (pilot + cost model even for a small batch)
+TIER_FLAGS = ([0, 2, 128, 128 | 64] + [64 | 8 | (t << 8) for t in range(5)]
               + [32 | 8 | (t << 8) for t in range(5)])
-TIER_IDS = (["auto", "warp_tier_only", "thread_pilot_cascade"]
+TIER_IDS = (["auto", "warp_tier_only", "pilot_cascade", "thread_pilot_cascade"]
             + [f"thread_k{w}" for w in (16, 24, 32, 48, 64)]
             + [f"group_k{w}" for w in (16, 24, 32, 48, 64)])
 
@@ -139,8 +140,9 @@ def _config_pool(xb, ds):
 
 
 @pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
-@pytest.mark.parametrize("flags", [0, 1, 2, 64, 32, 64 | 8, 64 | 8 | (2 << 8), 32 | 8, 32 | 8 | (2 << 8)],
-                         ids=["auto", "unsorted", "warp_tier_only", "thread_cascade", "group_cascade",
+@pytest.mark.parametrize("flags", [0, 1, 2, 128, 128 | 64, 32, 64 | 8, 64 | 8 | (2 << 8), 32 | 8,
+                                   32 | 8 | (2 << 8)],
+                         ids=["auto", "unsorted", "warp_tier_only", "pilot_cascade", "thread_cascade", "group_cascade",
                               "thread_from_k16", "thread_from_k32", "group_from_k16", "group_from_k32"])
 def test_configs_vs_reference_golden(xb, cfg, flags):
     from paper_2304_08662_b200 import synth
@@ -173,7 +175,9 @@ def test_configs_sample_vs_oracle_full_size(xb, oracle, cfg):
     assert result_rows_equal(out, exp).all()
     assert (ss == ess).all()
     a, _ = xb.extend_tasks(pool, ds.tasks, ds.k, ds.band)
-    for flags in (1, 32, 64):  # unsorted, lane groups throughout, one thread per unit
+    # unsorted, lane groups throughout, one thread per unit, and K16 starts whose
+    # escalations resume from saved records (past the record capacity on config 5)
+    for flags in (1, 32, 64, 64 | 8, 32 | 8):
         b, _ = xb.extend_tasks(pool, ds.tasks, ds.k, ds.band, exec_flags=flags)
         assert result_rows_equal(a, b).all(), flags
     # every sampled row inside the full run equals the sampled run
@@ -215,7 +219,8 @@ def test_self_extension_full_length(xb):
     assert len(set(right["delta_w"].tolist())) == 1
 
 
-@pytest.mark.parametrize("flags", [0, 32, 64, 64 | 8], ids=["auto", "group", "thread", "thread_from_k16"])
+@pytest.mark.parametrize("flags", [0, 32, 128 | 64, 64 | 8, 32 | 8],
+                         ids=["auto", "group", "thread_pilot", "thread_from_k16", "group_from_k16"])
 def test_band_failures_and_escalation(xb, oracle, flags):
     """Wide windows: X large so spreads exceed 32 and 64 slots (tier escalation)
     and a band small enough that some sides fail with exact spread/cells."""
