@@ -369,7 +369,9 @@ static int pool_device(xb_pool* p, int dev, cudaStream_t st, int64_t* h2d, DevPo
             CK(cudaMemcpyAsync(D.seq_len, p->seq_len.data(), size_t(n) * 8, cudaMemcpyHostToDevice, st));
         }
         CK(cudaMemcpyAsync(D.scheme, &p->dev_scheme, sizeof(DevScheme), cudaMemcpyHostToDevice, st));
-        CK(cudaStreamSynchronize(st));  // pageable sources above must outlive the copy
+        // the pinned words stream over PCIe while the host stages the tasks;
+        // batch creation waits for the stream before returning, so the pool
+        // cannot be repacked under an in-flight copy
         if (h2d) *h2d += p->n_words * 4 + n * 16 + int64_t(sizeof(DevScheme));
         D.ready = true;
     }
@@ -990,24 +992,46 @@ static int exec_devices(const xb_exec* ex, std::vector<int>& ids) {
     return XB_OK;
 }
 
+// align.cpp:271-279 order: any dangling id (first such task) before any seed
+// out of bounds (first such task); the scan runs on all host threads.
 static int validate_tasks(const xb_pool* p, const xb_task* tasks, int64_t n, int k, int64_t* bad) {
     const int64_t ns = xb_pool_size(p);
-    for (int64_t t = 0; t < n; ++t) {
-        const xb_task& q = tasks[t];
-        if (int64_t(q.h_id) >= ns || int64_t(q.v_id) >= ns) {  // align.cpp:271-273
-            if (bad) *bad = t;
-            return XB_E_DANGLING;
+    const int T = n > (1 << 16) ? n_host_threads() : 1;
+    const int64_t chunk = (n + T - 1) / std::max(T, 1);
+    std::vector<int64_t> first_dangling(size_t(std::max(T, 1)), INT64_MAX);
+    std::vector<int64_t> first_oob(size_t(std::max(T, 1)), INT64_MAX);
+    auto scan = [&](int c) {
+        const int64_t a = c * chunk, b = std::min(n, a + chunk);
+        for (int64_t t = a; t < b; ++t) {
+            const xb_task& q = tasks[t];
+            if (int64_t(q.h_id) >= ns || int64_t(q.v_id) >= ns) {
+                first_dangling[size_t(c)] = t;
+                return;  // nothing later in this chunk can matter
+            }
+            if (first_oob[size_t(c)] != INT64_MAX) continue;
+            const int64_t hl = p->offsets[q.h_id + 1] - p->offsets[q.h_id];
+            const int64_t vl = p->offsets[q.v_id + 1] - p->offsets[q.v_id];
+            if (int64_t(q.h_seed) + k > hl || int64_t(q.v_seed) + k > vl ||
+                q.h_seed > uint64_t(hl) || q.v_seed > uint64_t(vl))
+                first_oob[size_t(c)] = t;
         }
+    };
+    if (T <= 1) {
+        scan(0);
+    } else {
+        std::vector<std::thread> th;
+        for (int c = 0; c < T; ++c) th.emplace_back(scan, c);
+        for (auto& x : th) x.join();
     }
-    for (int64_t t = 0; t < n; ++t) {
-        const xb_task& q = tasks[t];
-        const int64_t hl = p->offsets[q.h_id + 1] - p->offsets[q.h_id];
-        const int64_t vl = p->offsets[q.v_id + 1] - p->offsets[q.v_id];
-        if (int64_t(q.h_seed) + k > hl || int64_t(q.v_seed) + k > vl ||  // align.cpp:276-279
-            q.h_seed > uint64_t(hl) || q.v_seed > uint64_t(vl)) {
-            if (bad) *bad = t;
-            return XB_E_SEED_OOB;
-        }
+    const int64_t dg = *std::min_element(first_dangling.begin(), first_dangling.end());
+    if (dg != INT64_MAX) {
+        if (bad) *bad = dg;
+        return XB_E_DANGLING;
+    }
+    const int64_t ob = *std::min_element(first_oob.begin(), first_oob.end());
+    if (ob != INT64_MAX) {
+        if (bad) *bad = ob;
+        return XB_E_SEED_OOB;
     }
     return XB_OK;
 }
@@ -1056,6 +1080,10 @@ xb_batch* xb_batch_create(xb_pool* p, const xb_task* tasks, int64_t n, int k, in
         if (rc) return fail(rc, B);
         rc = upload_inputs(B, D, tasks);
         if (rc) return fail(rc, B);
+    }
+    for (auto& D : B->devs) {  // pool + task uploads done (see pool_device)
+        if (cudaSetDevice(D.dev) != cudaSuccess || cudaStreamSynchronize(D.stream) != cudaSuccess)
+            return fail(XB_E_CUDA, B);
     }
     if (err) *err = XB_OK;
     return B;
