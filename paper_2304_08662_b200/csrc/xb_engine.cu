@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <cstdio>
 #include <cstring>
@@ -494,6 +495,15 @@ struct Workspace {
     DevResult* h_res = nullptr;
     int32_t* h_seed = nullptr;
     int64_t* h_tasks = nullptr;
+    // rows finished after the start tier (escalations, warp tier), gathered
+    // so that the bulk of the results can cross PCIe during the cascade tail
+    cudaStream_t copy_stream = nullptr;
+    int64_t capP = 0;
+    uint32_t* d_patch_idx = nullptr;
+    DevResult* d_patch_res = nullptr;
+    uint32_t* h_patch_idx = nullptr;
+    DevResult* h_patch_res = nullptr;
+    int32_t* h_misc = nullptr;  // pinned: start tier read back after the pilot
 
     void release_units() {
         cudaFree(d_units);
@@ -505,6 +515,15 @@ struct Workspace {
         cudaFree(d_lists);
         cudaFree(d_pilot);
         cudaFree(d_cub);
+        cudaFree(d_patch_idx);
+        cudaFree(d_patch_res);
+        if (h_patch_idx) cudaFreeHost(h_patch_idx);
+        if (h_patch_res) cudaFreeHost(h_patch_res);
+        d_patch_idx = nullptr;
+        d_patch_res = nullptr;
+        h_patch_idx = nullptr;
+        h_patch_res = nullptr;
+        capP = 0;
         if (h_res) cudaFreeHost(h_res);
         d_units = nullptr;
         d_keys = d_vals = d_keys2 = d_order = d_lists = nullptr;
@@ -533,9 +552,11 @@ struct Workspace {
         cudaFree(d_ctr);
         cudaFree(d_scratch);
         cudaFree(d_resume);
+        if (h_misc) cudaFreeHost(h_misc);
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
         if (stream) cudaStreamDestroy(stream);
+        if (copy_stream) cudaStreamDestroy(copy_stream);
     }
 };
 
@@ -551,6 +572,17 @@ static void destroy_workspaces(xb_pool* p) {
 struct DevBatch {
     int dev = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;
+    int t0 = -1;               // start tier, when known on the host
+    bool early_copy = false;   // results copied after the start tier, patched at fetch
+    int64_t capP = 0;
+    uint32_t* d_patch_idx = nullptr;
+    DevResult* d_patch_res = nullptr;
+    uint32_t* h_patch_idx = nullptr;
+    DevResult* h_patch_res = nullptr;
+    int32_t* h_misc = nullptr;
+    TierParams tp{};           // planned launch parameters (run_plan -> run_cascade)
+    bool all_group = false, no_group = false;
     Workspace* ws = nullptr;
     bool ws_cached = false;
     DevPool* pool = nullptr;
@@ -643,6 +675,8 @@ static int setup_device(xb_batch* B, DevBatch& D, const xb_exec* ex) {
         for (auto& e : W.ev) CK(cudaEventCreate(&e));
         CK(cudaMalloc(&W.d_ctr, sizeof(DevCounters)));
         CK(cudaMalloc(&W.d_resume, size_t(kResumeCap) * kResumeStride * 4));
+        CK(cudaStreamCreateWithFlags(&W.copy_stream, cudaStreamNonBlocking));
+        CK(cudaMallocHost(&W.h_misc, 64));
     }
     D.stream = (ex && ex->stream && B->devs.size() == 1) ? (cudaStream_t)ex->stream : W.stream;
     D.ev = W.ev;
@@ -664,6 +698,11 @@ static int setup_device(xb_batch* B, DevBatch& D, const xb_exec* ex) {
         CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, W.cub_bytes, W.d_keys, W.d_keys2,
                                                      W.d_vals, W.d_order, int(U), 0, 32, D.stream));
         CK(cudaMalloc(&W.d_cub, std::max<size_t>(W.cub_bytes, 16)));
+        W.capP = std::min<int64_t>(U, 1 << 20);
+        CK(cudaMalloc(&W.d_patch_idx, size_t(W.capP) * 4));
+        CK(cudaMalloc(&W.d_patch_res, size_t(W.capP) * sizeof(DevResult)));
+        CK(cudaMallocHost(&W.h_patch_idx, size_t(W.capP) * 4));
+        CK(cudaMallocHost(&W.h_patch_res, size_t(W.capP) * sizeof(DevResult)));
         W.capU = U;
     }
     const int64_t I = std::max<int64_t>(D.n_items, 1);
@@ -702,6 +741,13 @@ static int setup_device(xb_batch* B, DevBatch& D, const xb_exec* ex) {
     D.cub_bytes = W.cub_bytes;
     D.d_scratch = W.d_scratch;
     D.d_resume = W.d_resume;
+    D.copy_stream = W.copy_stream;
+    D.capP = W.capP;
+    D.d_patch_idx = W.d_patch_idx;
+    D.d_patch_res = W.d_patch_res;
+    D.h_patch_idx = W.h_patch_idx;
+    D.h_patch_res = W.h_patch_res;
+    D.h_misc = W.h_misc;
     D.h_res = W.h_res;
     D.d_tasks = W.d_tasks;
     D.d_seed = W.d_seed;
@@ -781,7 +827,7 @@ static int occupancy_blocks(bool group, int t, int mode, int* out) {
     return XB_OK;
 }
 
-static int run_device(xb_batch* B, DevBatch& D) {
+static int run_plan(xb_batch* B, DevBatch& D) {
     CK(cudaSetDevice(D.dev));
     xb_pool* p = B->pool;
     const int mode = p->dev_scheme.fast_dna ? 0 : (p->enc == ENC_2BIT ? 1 : 2);
@@ -790,6 +836,8 @@ static int run_device(xb_batch* B, DevBatch& D) {
     CK(cudaEventRecord(D.ev[0], D.stream));
     CK(cudaMemsetAsync(D.d_ctr, 0, sizeof(DevCounters), D.stream));
     const int64_t nu = D.n_units;
+    D.early_copy = false;
+    D.t0 = -1;
     if (nu == 0) {
         for (int q = 1; q < 9; ++q) CK(cudaEventRecord(D.ev[q], D.stream));
         return XB_OK;
@@ -910,24 +958,77 @@ static int run_device(xb_batch* B, DevBatch& D) {
     CK(cudaGetLastError());
     ++D.launches;
     CK(cudaEventRecord(D.ev[2], D.stream));
-    // ---- cascade: the start tier takes the queue, wider tiers their escalations ----
+    D.tp = tp;
+    D.all_group = all_group;
+    D.no_group = no_group;
+    D.t0 = forced >= 0 ? forced : (pn > 0 ? -1 : default_start);  // -1: read back after the pilot
+    if (D.t0 < 0)
+        CK(cudaMemcpyAsync(D.h_misc, &D.d_ctr->start_tier, 4, cudaMemcpyDeviceToHost, D.stream));
+    return XB_OK;
+}
+
+__global__ void gather_patch_kernel(TierParams P, int t0, uint32_t* __restrict__ idx,
+                                    DevResult* __restrict__ out, long long cap) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (int t = t0 + 1; t < kNumTiers; ++t) {
+        const long long len = (long long)P.ctr->list_len[t];
+        const uint32_t* L = P.lists + (long long)t * P.n_units;
+        for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += stride) {
+            const uint32_t e = L[i];
+            const uint32_t unit = (e & kResumeFlag)
+                                      ? uint32_t(P.resume[(long long)(e & ~kResumeFlag) * kResumeStride + kRecUnit])
+                                      : e;
+            const unsigned long long slot = atomicAdd(&P.ctr->patch_n, 1ull);
+            if ((long long)slot < cap) {
+                idx[slot] = unit;
+                out[slot] = P.results[unit];
+            }
+        }
+    }
+}
+
+// The cascade: the start tier takes the queue, wider tiers their
+// escalations, the warp tier whatever is left.  Once the start tier is done
+// every other row is final, so the results cross PCIe (copy stream) while
+// the wider tiers run; the rows finished later are gathered for a patch.
+static int run_cascade(xb_batch* B, DevBatch& D) {
+    if (D.n_units == 0) return XB_OK;
+    CK(cudaSetDevice(D.dev));
+    xb_pool* p = B->pool;
+    const int mode = D.mode;
+    if (D.t0 < 0) D.t0 = D.h_misc[0];  // the stream was synchronised by xb_batch_run
+    TierParams tp = D.tp;
     for (int t = 0; t < 5; ++t) {
         tp.tier = t;
-        if (all_group || no_group) {
-            tp.role = kRoleAll;
-            CK(launch_tier(all_group, mode, t, tp, D.sm_count * (all_group ? D.gocc[t] : D.occ[t]), D.stream));
-            ++D.launches;
-        } else {
-            tp.role = kRoleStart;
-            CK(launch_tier(false, mode, t, tp, D.sm_count * D.occ[t], D.stream));
-            ++D.launches;
-            if (t > 0) {
-                tp.role = kRoleEscalations;
-                CK(launch_tier(true, mode, t, tp, D.sm_count * D.gocc[t], D.stream));
+        if (t >= D.t0) {
+            if (D.all_group || D.no_group) {
+                tp.role = kRoleAll;
+                CK(launch_tier(D.all_group, mode, t, tp,
+                               D.sm_count * (D.all_group ? D.gocc[t] : D.occ[t]), D.stream));
                 ++D.launches;
+            } else {
+                tp.role = kRoleStart;
+                CK(launch_tier(false, mode, t, tp, D.sm_count * D.occ[t], D.stream));
+                ++D.launches;
+                if (t > D.t0) {
+                    tp.role = kRoleEscalations;
+                    CK(launch_tier(true, mode, t, tp, D.sm_count * D.gocc[t], D.stream));
+                    ++D.launches;
+                }
             }
         }
         CK(cudaEventRecord(D.ev[3 + t], D.stream));
+        if (t == D.t0 && D.capP > 0) {
+            CK(cudaStreamWaitEvent(D.copy_stream, D.ev[3 + t], 0));
+            CK(cudaMemcpyAsync(D.h_res, D.d_res, size_t(D.n_units) * sizeof(DevResult),
+                               cudaMemcpyDeviceToHost, D.copy_stream));
+            if (!B->units_mode && D.n_items)
+                CK(cudaMemcpyAsync(D.h_seed, D.d_seed, size_t(D.n_items) * 4, cudaMemcpyDeviceToHost,
+                                   D.copy_stream));
+            CK(cudaEventRecord(D.ev[11], D.copy_stream));
+            D.early_copy = true;
+            B->d2h += D.n_units * int64_t(sizeof(DevResult)) + (B->units_mode ? 0 : D.n_items * 4);
+        }
     }
     // ---- warp per unit: exact generic path for whatever is left ----
     {
@@ -941,11 +1042,18 @@ static int run_device(xb_batch* B, DevBatch& D) {
         ++D.launches;
     }
     CK(cudaEventRecord(D.ev[8], D.stream));
+    if (D.early_copy) {
+        gather_patch_kernel<<<unsigned(D.sm_count), 256, 0, D.stream>>>(tp, D.t0, D.d_patch_idx,
+                                                                       D.d_patch_res, D.capP);
+        CK(cudaGetLastError());
+        ++D.launches;
+    }
     return XB_OK;
 }
 
 static int fetch_device(xb_batch* B, DevBatch& D) {
     CK(cudaSetDevice(D.dev));
+    if (D.early_copy) return XB_OK;  // bulk copy already issued by run_cascade
     if (D.n_units)
         CK(cudaMemcpyAsync(D.h_res, D.d_res, size_t(D.n_units) * sizeof(DevResult),
                            cudaMemcpyDeviceToHost, D.stream));
@@ -1091,8 +1199,18 @@ xb_batch* xb_batch_create(xb_pool* p, const xb_task* tasks, int64_t n, int k, in
 
 int xb_batch_run(xb_batch* B) {
     if (!B) return XB_E_BAD_PARAM;
+    for (auto& D : B->devs) {  // prep, sort, pilot, start-tier choice on every device
+        const int rc = run_plan(B, D);
+        if (rc) return rc;
+    }
+    for (auto& D : B->devs) {  // a pilot-chosen start tier is read back (after ~1 ms)
+        if (D.n_units && D.t0 < 0) {
+            CK(cudaSetDevice(D.dev));
+            CK(cudaStreamSynchronize(D.stream));
+        }
+    }
     for (auto& D : B->devs) {
-        const int rc = run_device(B, D);
+        const int rc = run_cascade(B, D);
         if (rc) return rc;
     }
     B->ran = true;
@@ -1115,25 +1233,51 @@ int xb_batch_fetch(xb_batch* B, xb_side_result* out, int32_t* seed_score) {
     }
     for (auto& D : B->devs) {
         CK(cudaSetDevice(D.dev));
-        CK(cudaStreamSynchronize(D.stream));
         const bool sharded = B->devs.size() > 1;
-        if (B->units_mode) {
-            for (int64_t q = 0; q < D.n_units; ++q) {
-                const int64_t g = sharded ? D.tasks[size_t(q)] : q;
-                std::memcpy(&out[g], &D.h_res[q], sizeof(xb_side_result));
+        // local unit q -> caller's row
+        auto row = [&](int64_t q) -> int64_t {
+            if (B->units_mode) return sharded ? D.tasks[size_t(q)] : q;
+            return sharded ? 2 * D.tasks[size_t(q >> 1)] + (q & 1) : q;
+        };
+        auto copy_rows = [&](const DevResult* src) {
+            if (!sharded) {
+                parallel_for(D.n_units, [&](int64_t a, int64_t b) {
+                    std::memcpy(out + a, src + a, size_t(b - a) * sizeof(xb_side_result));
+                });
+            } else {
+                parallel_for(D.n_units, [&](int64_t a, int64_t b) {
+                    for (int64_t q = a; q < b; ++q) std::memcpy(&out[row(q)], &src[q], sizeof(xb_side_result));
+                });
             }
-        } else if (!sharded) {
-            const DevResult* src = D.h_res;
-            parallel_for(D.n_units, [&](int64_t a, int64_t b) {
-                std::memcpy(out + a, src + a, size_t(b - a) * sizeof(xb_side_result));
-            });
-            if (seed_score) std::memcpy(seed_score, D.h_seed, size_t(D.n_items) * 4);
-        } else {
-            for (int64_t q = 0; q < D.n_items; ++q) {
-                const int64_t g = D.tasks[size_t(q)];
-                std::memcpy(&out[2 * g], &D.h_res[2 * q], 2 * sizeof(xb_side_result));
-                if (seed_score) seed_score[g] = D.h_seed[q];
+        };
+        // bulk rows: on the host while the device may still be in the cascade tail
+        CK(cudaEventSynchronize(D.early_copy ? D.ev[11] : D.ev[9]));
+        copy_rows(D.h_res);
+        if (seed_score && !B->units_mode) {
+            if (!sharded)
+                std::memcpy(seed_score, D.h_seed, size_t(D.n_items) * 4);
+            else
+                for (int64_t q = 0; q < D.n_items; ++q) seed_score[D.tasks[size_t(q)]] = D.h_seed[q];
+        }
+        if (!D.early_copy) continue;
+        // rows finished after the start tier
+        CK(cudaStreamSynchronize(D.stream));
+        unsigned long long np = 0;
+        CK(cudaMemcpy(&np, &D.d_ctr->patch_n, 8, cudaMemcpyDeviceToHost));
+        B->d2h += 8;
+        if (int64_t(np) <= D.capP) {
+            if (np) {
+                CK(cudaMemcpy(D.h_patch_idx, D.d_patch_idx, size_t(np) * 4, cudaMemcpyDeviceToHost));
+                CK(cudaMemcpy(D.h_patch_res, D.d_patch_res, size_t(np) * sizeof(DevResult),
+                              cudaMemcpyDeviceToHost));
+                B->d2h += int64_t(np) * int64_t(4 + sizeof(DevResult));
             }
+            for (unsigned long long i = 0; i < np; ++i)
+                std::memcpy(&out[row(D.h_patch_idx[i])], &D.h_patch_res[i], sizeof(xb_side_result));
+        } else {  // more late rows than patch slots: copy everything again
+            CK(cudaMemcpy(D.h_res, D.d_res, size_t(D.n_units) * sizeof(DevResult), cudaMemcpyDeviceToHost));
+            B->d2h += D.n_units * int64_t(sizeof(DevResult));
+            copy_rows(D.h_res);
         }
     }
     return XB_OK;
@@ -1178,7 +1322,13 @@ int xb_batch_stats(xb_batch* B, xb_stats* st) {
 
 void xb_batch_free(xb_batch* B) {
     if (!B) return;
-    for (auto& D : B->devs) free_dev(B->pool, D);
+    for (auto& D : B->devs) {  // nothing may still write into a workspace handed back
+        if (D.ws && cudaSetDevice(D.dev) == cudaSuccess) {
+            if (D.stream) cudaStreamSynchronize(D.stream);
+            if (D.copy_stream) cudaStreamSynchronize(D.copy_stream);
+        }
+        free_dev(B->pool, D);
+    }
     delete B;
 }
 

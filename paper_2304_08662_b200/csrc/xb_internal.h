@@ -58,6 +58,7 @@ struct DevCounters {
     int32_t start_tier;                // chosen by the pilot
     int32_t pad;
     unsigned long long resume_next;    // resume records handed out
+    unsigned long long patch_n;        // result rows finalised after the start tier
 };
 
 // Resume records: a unit that outgrows its tier saves its band state at the
