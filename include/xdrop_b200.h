@@ -128,7 +128,7 @@ void xb_scheme_free(xb_scheme* s);
 
 /* ---- detached sequence pool (SequenceStore, sequence.hpp:13-19) ---- */
 /* Symbols are validated against the scheme alphabet and packed: 2 bits per
- * base when every sequence is pure ACGT, else 5-bit alphabet codes. */
+ * base when every sequence is pure ACGT, else one byte (alphabet code) per symbol. */
 xb_pool* xb_pool_create(const xb_scheme* s, int* err);
 /* returns the new dense id (>= 0) or -XB_E_* */
 int64_t xb_pool_add(xb_pool* p, const char* symbols, int64_t len);

@@ -1,5 +1,5 @@
 // Host side of the xdrop_b200 C-ABI: scoring schemes, the detached sequence
-// pool (2-bit / 5-bit packing, one upload per device), LR split + cost sort
+// pool (2-bit / byte packing, one upload per device), LR split + cost sort
 // on the device, the tier cascade, and LPT sharding across devices.
 // Reference interfaces replaced are cited per entry point in
 // include/xdrop_b200.h.
@@ -282,10 +282,10 @@ static bool thread_tiers_ok(const xb_pool* p) {
 static void pool_pack(xb_pool* p) {
     if (p->packed) return;
     const xb_scheme& s = p->scheme;
-    p->enc = (s.kind == 0 && p->all_acgt) ? ENC_2BIT : ENC_5BIT;
+    p->enc = (s.kind == 0 && p->all_acgt) ? ENC_2BIT : ENC_8BIT;
     const int64_t total = int64_t(p->symbols.size());
     const int64_t nsym = kPoolPad + total + kPoolPad;
-    p->n_words = p->enc == ENC_2BIT ? (nsym + 15) / 16 + 2 : (nsym + 5) / 6 + 2;
+    p->n_words = p->enc == ENC_2BIT ? (nsym + 15) / 16 + 2 : (nsym + 3) / 4 + 2;
     if (p->host_words) cudaFreeHost(p->host_words);
     if (cudaMallocHost(&p->host_words, size_t(p->n_words) * 4) != cudaSuccess) {
         cudaGetLastError();
@@ -303,8 +303,8 @@ static void pool_pack(xb_pool* p) {
     }
     const char* sym = p->symbols.data();
     uint32_t* W = p->host_words;
-    const int per = p->enc == ENC_2BIT ? 16 : 6;
-    const int bits = p->enc == ENC_2BIT ? 2 : 5;
+    const int per = p->enc == ENC_2BIT ? 16 : 4;
+    const int bits = p->enc == ENC_2BIT ? 2 : 8;
     parallel_for(p->n_words, [&](int64_t a, int64_t b) {
         for (int64_t w = a; w < b; ++w) {
             uint32_t acc = 0;
@@ -451,7 +451,7 @@ int64_t xb_pool_seq_len(const xb_pool* p, int64_t id) {
 }
 
 int xb_pool_bits_per_symbol(const xb_pool* p) {
-    return (p->scheme.kind == 0 && p->all_acgt) ? 2 : 5;
+    return (p->scheme.kind == 0 && p->all_acgt) ? 2 : 8;
 }
 
 void xb_pool_evict(xb_pool* p) {
@@ -1037,7 +1037,7 @@ static int run_cascade(xb_batch* B, DevBatch& D) {
         if (p->enc == ENC_2BIT)
             warp_tier_kernel<ENC_2BIT><<<blocks, 128, 0, D.stream>>>(tp);
         else
-            warp_tier_kernel<ENC_5BIT><<<blocks, 128, 0, D.stream>>>(tp);
+            warp_tier_kernel<ENC_8BIT><<<blocks, 128, 0, D.stream>>>(tp);
         CK(cudaGetLastError());
         ++D.launches;
     }

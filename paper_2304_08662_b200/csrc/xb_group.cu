@@ -61,8 +61,10 @@ struct GState {
     int32_t Tc, best_d, best_u, cells, delta_w;
     uint32_t VW, HW;             // 2-bit windows of this lane's S slots (MODE 0)
     uint32_t VWb[NB], HWb[NB];   // byte windows (table modes)
-    Reader<true> rv;             // lane 0: v symbols entering slot 0
-    Reader<false> rh;            // lane G-1: h symbols entering slot K-1
+    static constexpr int RENC = MODE == 2 ? ENC_8BIT : ENC_2BIT;  // pool encoding read
+    static constexpr int RPER = EncFields<RENC>::PER;              // refill period (iterations)
+    Reader<true, RENC> rv;       // lane 0: v symbols entering slot 0
+    Reader<false, RENC> rh;      // lane G-1: h symbols entering slot K-1
 };
 
 template <int K, int G, int MODE>
@@ -86,7 +88,7 @@ __device__ __forceinline__ void g_windows(GState<K, G, MODE>& S, const uint32_t*
         if (lane == 0) S.rv.init(pool, S.v_pos, S.vdir, a + 1, rv_r);
         if (lane == G - 1) S.rh.init(pool, S.h_pos, S.hdir, b + K, rh_r);
     } else {
-        constexpr int ENC = MODE == 1 ? ENC_2BIT : ENC_5BIT;
+        constexpr int ENC = MODE == 1 ? ENC_2BIT : ENC_8BIT;
 #pragma unroll
         for (int r = 0; r < GState<K, G, MODE>::NB; ++r) {
             uint32_t vw = 0, hw = 0;
@@ -101,6 +103,26 @@ __device__ __forceinline__ void g_windows(GState<K, G, MODE>& S, const uint32_t*
             S.VWb[r] = vw;
             S.HWb[r] = hw;
         }
+        if (lane == 0) S.rv.init(pool, S.v_pos, S.vdir, a + 1, rv_r);
+        if (lane == G - 1) S.rh.init(pool, S.h_pos, S.hdir, b + K, rh_r);
+    }
+}
+
+// Table modes: sentinel bytes over this lane's slots whose v or h symbol lies
+// past the view's end (see the thread tier's sentinel_windows).
+template <int K, int G, int MODE>
+__device__ __forceinline__ void g_sentinels(GState<K, G, MODE>& S, int d, int k0) {
+    using St = GState<K, G, MODE>;
+    const int fd = d >> 1, cd = d - fd;
+    const int vhi = fd - S.ubase - 1 - S.n - k0;  // lane slots 0..vhi: v index >= n
+    const int hlo = S.m - (cd + S.ubase - 1) - k0;  // lane slots hlo..: h index >= m
+#pragma unroll
+    for (int r = 0; r < St::NB; ++r) {
+        const int v1 = min(vhi - 4 * r, 3), h0 = max(hlo - 4 * r, 0);
+        const uint32_t mv = v1 < 0 ? 0u : gbits(0, 8 * v1 + 7);
+        const uint32_t mh = h0 > 3 ? 0u : gbits(8 * h0, 31);
+        S.VWb[r] = (S.VWb[r] & ~mv) | (0x1F1F1F1Fu & mv);
+        S.HWb[r] = (S.HWb[r] & ~mh) | (0x1F1F1F1Fu & mh);
     }
 }
 
@@ -158,22 +180,19 @@ __device__ __forceinline__ void gfeed(GState<K, G, MODE>& S, const TierParams& P
             S.HW = (S.HW >> 2) | (in << (2 * (SS - 1)));
         }
     } else {
-        constexpr int ENC = MODE == 1 ? ENC_2BIT : ENC_5BIT;
         constexpr int NB = St::NB;
         constexpr int top = 8 * ((SS - 1) & 3);  // bit offset of slot SS-1 in its word
-        const int fd = d >> 1;
         if constexpr (ODD) {
             const uint32_t out = (S.VWb[NB - 1] >> top) & 0xFFu;
             uint32_t in = __shfl_up_sync(gmask, out, 1, G);
-            if (lane == 0) in = code_at<ENC>(P.pool, S.v_pos, S.vdir, S.n, int64_t(fd) - S.ubase);
+            if (lane == 0) in = S.rv.take();
 #pragma unroll
             for (int r = NB - 1; r > 0; --r) S.VWb[r] = __funnelshift_l(S.VWb[r - 1], S.VWb[r], 8);
             S.VWb[0] = (S.VWb[0] << 8) | in;
         } else {
             const uint32_t out = S.HWb[0] & 0xFFu;
             uint32_t in = __shfl_down_sync(gmask, out, 1, G);
-            if (lane == G - 1)
-                in = code_at<ENC>(P.pool, S.h_pos, S.hdir, S.m, int64_t(d - fd) + S.ubase - 1 + K);
+            if (lane == G - 1) in = S.rh.take();
 #pragma unroll
             for (int r = 0; r < NB - 1; ++r) S.HWb[r] = __funnelshift_r(S.HWb[r], S.HWb[r + 1], 8);
             const uint32_t keep = top == 24 ? 0xFFFFFFFFu : ((1u << (top + 8)) - 1u);
@@ -323,7 +342,8 @@ __device__ __forceinline__ void gstep(GState<K, G, MODE>& S, int32_t (&cur)[K / 
                         }
                         A -= sh;
                         g_limits(S);
-                        const int to_refill = 16 - int(it & 15);
+                        constexpr int PER = St::RPER;
+                        const int to_refill = PER - int(it & (PER - 1));
                         g_windows(S, P.pool, lane, ODD ? to_refill : to_refill - 1, to_refill);
                     }
                 }
@@ -332,7 +352,10 @@ __device__ __forceinline__ void gstep(GState<K, G, MODE>& S, int32_t (&cur)[K / 
                     const int khi = S.m - (d - fd) - S.ubase;
                     const int l = max(klo - k0, 0), h = min(min(khi, K - 1) - k0, SS - 1);
                     vml = gbits(l, h);
-                    inv = ~((l > h) ? 0u : gbits(2 * l, 2 * h + 1));
+                    if constexpr (MODE == 0)
+                        inv = ~((l > h) ? 0u : gbits(2 * l, 2 * h + 1));
+                    else
+                        g_sentinels(S, d, k0);
                 }
                 wm1 = max(w, 0) - 1;
             }
@@ -497,6 +520,11 @@ __global__ void __launch_bounds__(128) group_tier_kernel(TierParams P) {
     S.m = S.n = 0;
     S.stop = kDone;
     S.VW = S.HW = 0u;
+    // a group that never gets a unit still feeds its windows from its readers
+    // (table modes index the shared table with those codes): start them empty
+    S.rv.cur = S.rh.cur = 0u;
+    S.rv.w0 = S.rv.w1 = S.rh.w0 = S.rh.w1 = 0u;
+    S.rv.sh = S.rh.sh = 0u;
 #pragma unroll
     for (int r = 0; r < St::NB; ++r) S.VWb[r] = S.HWb[r] = 0u;
     int32_t E[SS], O[SS];
@@ -537,7 +565,7 @@ __global__ void __launch_bounds__(128) group_tier_kernel(TierParams P) {
             S.vdir = (u.dir >> 1) & 1;
             S.dcap = P.pilot ? P.pilot_cap : (INT_MAX >> 1);
             S.stop = 0;
-            const int r = 15 - int(it & 15);
+            const int r = (St::RPER - 1) - int(it & (St::RPER - 1));
             if (!rec) {
                 S.d = 1;
                 S.ubase = -(K / 2);
@@ -593,11 +621,9 @@ __global__ void __launch_bounds__(128) group_tier_kernel(TierParams P) {
     fetch();
     it = 0;
     while (__any_sync(0xFFFFFFFFu, active)) {
-        if constexpr (MODE == 0) {
-            if (active && (it & 15) == 0) {
-                if (lane == 0) S.rv.refill(P.pool);
-                if (lane == G - 1) S.rh.refill(P.pool);
-            }
+        if (active && (it & (St::RPER - 1)) == 0) {
+            if (lane == 0) S.rv.refill(P.pool);
+            if (lane == G - 1) S.rh.refill(P.pool);
         }
         const bool peel = active && !(S.d & 1);
         if (__any_sync(0xFFFFFFFFu, peel)) {  // rare: some group resumed at an even d

@@ -6,8 +6,9 @@
 namespace xb {
 
 // Pool encodings. ENC_2BIT: pure ACGT, codes A0 C1 G2 T3, 16 symbols per
-// 32-bit word. ENC_5BIT: alphabet index, 6 codes per word (bits 0..29).
-enum : int { ENC_2BIT = 2, ENC_5BIT = 5 };
+// 32-bit word. ENC_8BIT: alphabet index (< 32) in a byte, 4 per word, so a
+// view streams through the same aligned-chunk readers as 2-bit DNA.
+enum : int { ENC_2BIT = 2, ENC_8BIT = 8 };
 
 // symbols of zero padding in front of / behind every device pool, so window
 // fetches that run past a sequence (masked out later) never leave the buffer

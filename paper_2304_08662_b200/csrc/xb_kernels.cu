@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(128) warp_tier_kernel(TierParams P) {
 }
 
 template __global__ void warp_tier_kernel<ENC_2BIT>(TierParams);
-template __global__ void warp_tier_kernel<ENC_5BIT>(TierParams);
+template __global__ void warp_tier_kernel<ENC_8BIT>(TierParams);
 
 // ----------------------------------------------------------------- prep ----
 // LR split (partition.cpp:45-81) + checked seed score (align.cpp:283-285)
@@ -235,8 +235,8 @@ __global__ void prep_kernel(PrepParams P) {
             hc = code_at<ENC_2BIT>(P.pool, hb + hs, 1, 1ll << 40, i);
             vc = code_at<ENC_2BIT>(P.pool, vb + vs, 1, 1ll << 40, i);
         } else {
-            hc = code_at<ENC_5BIT>(P.pool, hb + hs, 1, 1ll << 40, i);
-            vc = code_at<ENC_5BIT>(P.pool, vb + vs, 1, 1ll << 40, i);
+            hc = code_at<ENC_8BIT>(P.pool, hb + hs, 1, 1ll << 40, i);
+            vc = code_at<ENC_8BIT>(P.pool, vb + vs, 1, 1ll << 40, i);
         }
         ss += P.scheme->sim[hc * 32 + vc];  // sim(h symbol, v symbol)
     }

@@ -109,18 +109,44 @@ __device__ __forceinline__ uint32_t code_at(const uint32_t* __restrict__ pool, i
     if (t < 0 || t >= len) return kSentinel;
     const int64_t p = dir ? pos + t : pos - t;
     if (ENC == ENC_2BIT) return (ldw(pool, p >> 4) >> (uint32_t(p & 15) * 2u)) & 3u;
-    const uint64_t up = uint64_t(p);
-    const uint64_t wi = up / 6u;
-    return (ldw(pool, int64_t(wi)) >> (uint32_t(up - wi * 6u) * 5u)) & 31u;
+    return (ldw(pool, p >> 2) >> (uint32_t(p & 3) * 8u)) & 0xFFu;
 }
 
-// Streams consecutive 16-symbol chunks of a 2-bit view.  Refills happen at
-// warp-uniform loop iterations (every 16), so no thread diverges for them:
-// `cur` is filled at (re)initialisation with the symbols needed up to the
-// next refill point, and each refill assembles the chunk whose words were
-// loaded one refill (16 iterations) earlier.  TOP = chunks top-first (v side).
-template <bool TOP>
+// field geometry of an encoding: PER symbols of BITS bits per 32-bit word
+template <int ENC>
+struct EncFields {
+    static constexpr int BITS = ENC == ENC_2BIT ? 2 : 8;
+    static constexpr int PER = 32 / BITS;
+    static constexpr int LOG = ENC == ENC_2BIT ? 4 : 2;
+};
+
+// exact reversal of the fields of a word
+template <int ENC>
+__device__ __forceinline__ uint32_t rev_fields(uint32_t x) {
+    if constexpr (ENC == ENC_2BIT)
+        return rev16(x);
+    else
+        return __byte_perm(x, 0u, 0x0123);
+}
+
+// PER symbols starting at pool symbol position q, lowest address in field 0
+template <int ENC>
+__device__ __forceinline__ uint32_t chunk_mem_e(const uint32_t* __restrict__ pool, int64_t q) {
+    using F = EncFields<ENC>;
+    const int64_t wi = q >> F::LOG;
+    const uint32_t sh = uint32_t(q & (F::PER - 1)) * uint32_t(F::BITS);
+    return __funnelshift_r(ldw(pool, wi), ldw(pool, wi + 1), sh);
+}
+
+// Streams consecutive PER-symbol chunks of a view.  Refills happen at
+// warp-uniform loop iterations (every PER: 16 for 2-bit, 4 for bytes), so no
+// thread diverges for them: `cur` is filled at (re)initialisation with the
+// symbols needed up to the next refill point, and each refill assembles the
+// chunk whose words were loaded one refill earlier.  TOP = chunks top-first
+// (v side: consume from the top field), else bottom-first (h side).
+template <bool TOP, int ENC = ENC_2BIT>
 struct Reader {
+    using F = EncFields<ENC>;
     uint32_t cur;   // remaining symbols until the next refill point
     uint32_t w0, w1;
     int64_t wnext;  // word index of the next load
@@ -131,10 +157,11 @@ struct Reader {
     // before the next refill point
     __device__ __forceinline__ void init(const uint32_t* pool, int64_t pos, int d, int64_t t0, int r) {
         dir = d;
-        cur = TOP ? chunk_tf(pool, pos, d, t0) : chunk_bf(pool, pos, d, t0);
-        const int64_t q = d ? pos + t0 + r : pos - (t0 + r) - 15;
-        const int64_t wi = q >> 4;
-        sh = uint32_t(q & 15) * 2u;
+        const uint32_t c = chunk_mem_e<ENC>(pool, d ? pos + t0 : pos - t0 - (F::PER - 1));
+        cur = (TOP ? (d != 0) : (d == 0)) ? rev_fields<ENC>(c) : c;
+        const int64_t q = d ? pos + t0 + r : pos - (t0 + r) - (F::PER - 1);
+        const int64_t wi = q >> F::LOG;
+        sh = uint32_t(q & (F::PER - 1)) * uint32_t(F::BITS);
         w0 = ldw(pool, wi);
         w1 = ldw(pool, wi + 1);
         wnext = d ? wi + 2 : wi - 1;
@@ -142,13 +169,25 @@ struct Reader {
     __device__ __forceinline__ void refill(const uint32_t* pool) {
         const uint32_t c = __funnelshift_r(w0, w1, sh);
         const bool rev = TOP ? (dir != 0) : (dir == 0);
-        cur = rev ? rev16(c) : c;
+        cur = rev ? rev_fields<ENC>(c) : c;
         const uint32_t nw = ldw(pool, wnext);
         const bool fwd = dir != 0;
         const uint32_t o0 = w0, o1 = w1;
         w0 = fwd ? o1 : nw;
         w1 = fwd ? nw : o0;
         wnext += fwd ? 1 : -1;
+    }
+    // the next symbol's code (v side: TOP, h side: !TOP)
+    __device__ __forceinline__ uint32_t take() {
+        uint32_t c;
+        if constexpr (TOP) {
+            c = cur >> (32 - F::BITS);
+            cur <<= F::BITS;
+        } else {
+            c = cur & ((1u << F::BITS) - 1u);
+            cur >>= F::BITS;
+        }
+        return c;
     }
 };
 
@@ -176,8 +215,10 @@ struct TState {
     // windows
     uint32_t VW[MODE == 0 ? NW : NB];
     uint32_t HW[MODE == 0 ? NW : NB];
-    Reader<true> rv;
-    Reader<false> rh;
+    static constexpr int RENC = MODE == 2 ? ENC_8BIT : ENC_2BIT;  // pool encoding read
+    static constexpr int RPER = EncFields<RENC>::PER;              // refill period (iterations)
+    Reader<true, RENC> rv;
+    Reader<false, RENC> rh;
 };
 
 // LR split + seed score + cost keys, one thread per task

@@ -64,7 +64,7 @@ __device__ __forceinline__ void init_windows(TState<K, MODE>& S, const uint32_t*
         S.rv.init(pool, S.v_pos, S.vdir, a + 1, rv_r);
         S.rh.init(pool, S.h_pos, S.hdir, b + St::WK, rh_r);
     } else {
-        constexpr int ENC = MODE == 1 ? ENC_2BIT : ENC_5BIT;
+        constexpr int ENC = MODE == 1 ? ENC_2BIT : ENC_8BIT;
 #pragma unroll
         for (int r = 0; r < St::NB; ++r) {
             uint32_t vw = 0, hw = 0;
@@ -77,6 +77,30 @@ __device__ __forceinline__ void init_windows(TState<K, MODE>& S, const uint32_t*
             S.VW[r] = vw;
             S.HW[r] = hw;
         }
+        S.rv.init(pool, S.v_pos, S.vdir, a + 1, rv_r);
+        S.rh.init(pool, S.h_pos, S.hdir, b + St::WK, rh_r);
+    }
+}
+
+// Table modes stream symbols without bounds checks, so once the band reaches
+// past the matrix (d >= d_vm) the window bytes of slots whose v or h symbol
+// lies past the view's end are overwritten with the sentinel code on every
+// such step (its table row and column score -128: those cells never win).
+template <int K, int MODE>
+__device__ __forceinline__ void sentinel_windows(TState<K, MODE>& S, int d) {
+    using St = TState<K, MODE>;
+    const int fd = d >> 1, cd = d - fd;
+    const int a = fd - S.ubase - 1;  // v index of slot 0
+    const int b = cd + S.ubase - 1;  // h index of slot 0
+    const int vhi = a - S.n;         // slots 0..vhi: v index >= n
+    const int hlo = S.m - b;         // slots hlo..: h index >= m
+#pragma unroll
+    for (int r = 0; r < St::NB; ++r) {
+        const int v1 = min(vhi - 4 * r, 3), h0 = max(hlo - 4 * r, 0);
+        const uint32_t mv = v1 < 0 ? 0u : range_bits(0, 8 * v1 + 7);
+        const uint32_t mh = h0 > 3 ? 0u : range_bits(8 * h0, 31);
+        S.VW[r] = (S.VW[r] & ~mv) | (0x1F1F1F1Fu & mv);
+        S.HW[r] = (S.HW[r] & ~mh) | (0x1F1F1F1Fu & mh);
     }
 }
 
@@ -120,7 +144,8 @@ __device__ __forceinline__ void start_unit(TState<K, MODE>& S, int32_t (&E)[K], 
         E[k] = (k == K / 2) ? X + 1 : kDeadS;  // s(0,0) = 0 + 0 + off
     }
     // started at the end of iteration it: consumption begins next iteration
-    const int r = 15 - int(it & 15);
+    constexpr int PER = TState<K, MODE>::RPER;
+    const int r = (PER - 1) - int(it & (PER - 1));
     init_windows(S, P.pool, r, r);
 }
 
@@ -158,7 +183,8 @@ __device__ __forceinline__ void resume_unit(TState<K, MODE>& S, int32_t (&E)[K],
         O[k] = odd ? vc : vp;
         E[k] = odd ? vp : vc;
     }
-    const int r = 15 - int(it & 15);
+    constexpr int PER = TState<K, MODE>::RPER;
+    const int r = (PER - 1) - int(it & (PER - 1));
     S.d = odd ? d : d - 1;
     init_windows(S, P.pool, r, r);
     S.d = d;
@@ -269,8 +295,7 @@ __device__ __forceinline__ void feed(TState<K, MODE>& S, const TierParams& P, in
             S.VW[0] = __funnelshift_l(S.rv.cur, S.VW[0], 2);
             S.rv.cur <<= 2;
         } else {
-            constexpr int ENC = MODE == 1 ? ENC_2BIT : ENC_5BIT;
-            const uint32_t code = code_at<ENC>(P.pool, S.v_pos, S.vdir, S.n, int64_t(d >> 1) - S.ubase);
+            const uint32_t code = S.rv.take();
 #pragma unroll
             for (int r = St::NB - 1; r > 0; --r) S.VW[r] = __funnelshift_l(S.VW[r - 1], S.VW[r], 8);
             S.VW[0] = (S.VW[0] << 8) | code;
@@ -282,9 +307,7 @@ __device__ __forceinline__ void feed(TState<K, MODE>& S, const TierParams& P, in
             S.HW[St::NW - 1] = __funnelshift_r(S.HW[St::NW - 1], S.rh.cur, 2);
             S.rh.cur >>= 2;
         } else {
-            constexpr int ENC = MODE == 1 ? ENC_2BIT : ENC_5BIT;
-            const uint32_t code =
-                code_at<ENC>(P.pool, S.h_pos, S.hdir, S.m, int64_t(d - (d >> 1)) + S.ubase - 1 + St::WK);
+            const uint32_t code = S.rh.take();
 #pragma unroll
             for (int r = 0; r < St::NB - 1; ++r) S.HW[r] = __funnelshift_r(S.HW[r], S.HW[r + 1], 8);
             S.HW[St::NB - 1] = __funnelshift_r(S.HW[St::NB - 1], code, 8);
@@ -471,7 +494,8 @@ __device__ __forceinline__ void xstep(TState<K, MODE>& S, int32_t (&cur)[K], int
                         set_limits(S);
                         // symbols left to consume before the next refill (iteration multiple
                         // of 16): this iteration's own consumption counts unless it happened
-                        const int to_refill = 16 - int(it & 15);
+                        constexpr int PER = St::RPER;
+                        const int to_refill = PER - int(it & (PER - 1));
                         init_windows(S, P.pool, ODD ? to_refill : to_refill - 1, to_refill);
                     }
                 }
@@ -484,10 +508,14 @@ __device__ __forceinline__ void xstep(TState<K, MODE>& S, int32_t (&cur)[K], int
 #pragma unroll
                     for (int q = 0; q < St::NM; ++q)
                         vm[q] = range_bits(max(klo - 32 * q, 0), min(khk - 32 * q, 31));
+                    if constexpr (MODE == 0) {
 #pragma unroll
-                    for (int ww = 0; ww < St::NW; ++ww) {
-                        const int l = max(klo - 16 * ww, 0), h = min(khi - 16 * ww, 15);
-                        inv[ww] = ~range_bits(2 * l, 2 * h + 1);
+                        for (int ww = 0; ww < St::NW; ++ww) {
+                            const int l = max(klo - 16 * ww, 0), h = min(khi - 16 * ww, 15);
+                            inv[ww] = ~range_bits(2 * l, 2 * h + 1);
+                        }
+                    } else {
+                        sentinel_windows(S, d);
                     }
                 }
                 wm1 = max(w, 0) - 1;  // a clamped-empty row counts no cells (align.cpp:84-90)
@@ -554,11 +582,14 @@ __device__ __forceinline__ void xstep(TState<K, MODE>& S, int32_t (&cur)[K], int
 }
 
 // resident blocks per SM the register budget is sized for
-template <int K>
-constexpr int tier_min_blocks() { return K <= 24 ? 4 : K <= 32 ? 3 : 2; }
+// (table modes hold two more readers' worth of state: one block fewer from K24)
+template <int K, int MODE>
+constexpr int tier_min_blocks() {
+    return MODE == 0 ? (K <= 24 ? 4 : K <= 32 ? 3 : 2) : (K <= 16 ? 4 : K <= 24 ? 3 : 2);
+}
 
 template <int K, int MODE>
-__global__ void __launch_bounds__(kTB, tier_min_blocks<K>()) thread_tier_kernel(TierParams P) {
+__global__ void __launch_bounds__(kTB, tier_min_blocks<K, MODE>()) thread_tier_kernel(TierParams P) {
     __shared__ int8_t tab[MODE == 0 ? 4 : 32 * 256];
     const int32_t gap = P.scheme->gap, X = P.scheme->x;
     Queue Q;
@@ -619,11 +650,9 @@ __global__ void __launch_bounds__(kTB, tier_min_blocks<K>()) thread_tier_kernel(
 
     while (__any_sync(0xFFFFFFFFu, active)) {
         if (active) {
-            if constexpr (MODE == 0) {
-                if ((it & 15) == 0) {  // the same iteration for every thread
-                    S.rv.refill(P.pool);
-                    S.rh.refill(P.pool);
-                }
+            if ((it & (TState<K, MODE>::RPER - 1)) == 0) {  // the same iteration for every thread
+                S.rv.refill(P.pool);
+                S.rh.refill(P.pool);
             }
             // iterations start on odd d, except right after a resume at an even
             // d, where the odd half only feeds its v symbol

@@ -12,7 +12,7 @@ for c in ${CONFIGS:-5}; do
 done > gpurun_out/q_prof.log 2>&1
 cat gpurun_out/q_tests.log gpurun_out/q_prof.log
 if [ -n "$NCU" ] && [ $ok = 1 ]; then
-  ncu --set full --import-source on --clock-control none -k regex:thread_tier_kernel --launch-skip 2 -c 1 \
+  ncu --set full --import-source on --clock-control none -k regex:thread_tier_kernel --launch-skip 1 -c 1 \
     -o gpurun_out/q_k24 -f python scripts/prof_run.py --config 5 --scale 0.2 --runs 1 --flags 64 > gpurun_out/q_ncu.log 2>&1
   tail -2 gpurun_out/q_ncu.log
 fi

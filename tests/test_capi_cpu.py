@@ -58,7 +58,7 @@ def test_pool_packing_choice_and_validation():
     p = xb.DevicePool(s, b"ACGTACGT", np.array([0, 4, 8]))
     assert p.bits_per_symbol == 2
     p2 = xb.DevicePool(s, b"ACGNACGT", np.array([0, 4, 8]))
-    assert p2.bits_per_symbol == 5
+    assert p2.bits_per_symbol == 8
     with pytest.raises(xb.UnknownSymbol):
         xb.DevicePool(s, b"ACGUACGT", np.array([0, 4, 8]))
     with pytest.raises(xb.UnknownSymbol):
