@@ -10,6 +10,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -196,6 +197,26 @@ inline SeedAlignment extend_seed(SequencePool& pool, const ExtensionTask& task, 
     a.seed_score = ss;
     a.total = a.left.score + ss + a.right.score;
     return a;
+}
+
+// sweep_band (pipeline.hpp:58, pipeline.cpp:181-208): the band survey TSV.
+inline std::string sweep_band(size_t length, const std::vector<int>& xs,
+                              const std::vector<double>& p_grid, uint64_t rng_seed,
+                              const xb_exec* exec = nullptr) {
+    std::vector<int32_t> dw(xs.size() * p_grid.size());
+    std::vector<int32_t> x32(xs.begin(), xs.end());
+    check(xb_sweep_band(length, x32.data(), int32_t(xs.size()), p_grid.data(), int32_t(p_grid.size()),
+                        rng_seed, dw.data(), exec),
+          "sweep_band");
+    std::string out = "x\terror_rate\tdelta_w\n";
+    char buf[64];
+    for (size_t a = 0; a < xs.size(); ++a)
+        for (size_t b = 0; b < p_grid.size(); ++b) {
+            std::snprintf(buf, sizeof buf, "%d\t%.2f\t%d\n", xs[a], 1.0 - p_grid[b],
+                          dw[a * p_grid.size() + b]);
+            out += buf;
+        }
+    return out;
 }
 
 }  // namespace xband_b200

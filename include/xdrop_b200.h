@@ -102,6 +102,8 @@ typedef struct {
     int32_t sm_count;
     int32_t start_tier;          /* tier the pilot chose */
     int64_t dbg[6];              /* instrumented builds only (-DXB_COUNTERS=1), else 0 */
+    int32_t start_lane_groups;   /* 1: the start tier ran as lane groups (latency-bound batch) */
+    int32_t reserved;
 } xb_stats;
 
 typedef struct xb_scheme xb_scheme;
@@ -188,6 +190,23 @@ void xb_synth_sizes(const xb_synth* s, int64_t* sizes6);
 /* symbols: total bytes; offsets: n_seqs+1; tasks: 4*n_tasks int64 (h_id, v_id, h_seed, v_seed) */
 void xb_synth_copy(const xb_synth* s, char* symbols, int64_t* offsets, int64_t* tasks);
 void xb_synth_free(xb_synth* s);
+/* The reference's pair generator (generate_synthetic, proj/src/io.cpp:198-255,
+ * SynthParams io.hpp:35-42): `pairs` pairs of length `length`, V mutated at
+ * rate 1 - p_match outside a k-mer seed at the centre (uniform_seed = 0) or a
+ * uniform position; byte-identical to the reference for the same parameters.
+ * k < 1 or k > length: XB_E_BAD_PARAM (the reference's InputError). */
+xb_synth* xb_synth_pairs(uint64_t pairs, uint64_t length, double p_match, int k, int uniform_seed,
+                         uint64_t rng_seed, int* err);
+
+/* ---- band survey (sweep_band, proj/src/pipeline.cpp:181-208) ---- */
+/* For every X in xs and every p in ps: one synthetic pair (xb_synth_pairs
+ * with pairs = 1, k = 17, centred seed, rng_seed), extended over the full
+ * views with +1/-1/-1 scoring and band = length + 1; delta_w[ix*np + ip]
+ * receives its delta_w.  The X values run as concurrent batches.  The
+ * reference prints "x\terror_rate\tdelta_w" rows with error_rate = 1 - p
+ * as %.2f (xband_b200::sweep_band and xband.sweep_band reproduce the text). */
+int xb_sweep_band(uint64_t length, const int32_t* xs, int32_t nx, const double* ps, int32_t np,
+                  uint64_t rng_seed, int32_t* delta_w, const xb_exec* exec);
 
 #ifdef __cplusplus
 }

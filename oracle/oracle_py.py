@@ -250,6 +250,19 @@ class Ref:
                                         int(uniform_seed), buf, cap, C.byref(ec))
         return ec.value, buf.raw[:n].decode()
 
+    def sweep_band(self, length, xs, ps, seed=42) -> str:
+        """The reference's band survey TSV (pipeline.cpp:181-208)."""
+        xa = np.ascontiguousarray(xs, dtype=np.int32)
+        pa = np.ascontiguousarray(ps, dtype=np.float64)
+        f = self.lib.ref_sweep_band
+        f.restype = C.c_int64
+        f.argtypes = [C.c_int64, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_uint64, C.c_void_p,
+                      C.c_int64]
+        n = f(length, xa.ctypes.data, len(xa), pa.ctypes.data, len(pa), seed, None, 0)
+        buf = C.create_string_buffer(int(n) + 1)
+        f(length, xa.ctypes.data, len(xa), pa.ctypes.data, len(pa), seed, buf, n)
+        return buf.raw[:n].decode()
+
     def generate_synthetic(self, pairs, length, p_match, k=17, seed=42, uniform_seed=False):
         sym = np.zeros(2 * pairs * length + 1, dtype=np.uint8)
         off = np.zeros(2 * pairs + 1, dtype=np.int64)

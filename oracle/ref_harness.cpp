@@ -13,6 +13,7 @@
  * sides through xdrop_extend with one BandBuffers scratch per thread, which
  * the reference declares re-entrant (proj/include/xband/align.hpp:53-56).
  */
+#include <algorithm>
 #include <atomic>
 #include <cstdint>
 #include <cstring>
@@ -285,6 +286,17 @@ int64_t ref_generate_synthetic(int64_t pairs, int64_t length, double p_match, in
         tasks[4 * t + 3] = int64_t(ds.tasks[t].v_seed);
     }
     return int64_t(ds.tasks.size());
+}
+
+/* the reference's band survey (pipeline.cpp:181-208): TSV x / error_rate / delta_w */
+int64_t ref_sweep_band(int64_t length, const int* xs, int nx, const double* ps, int np,
+                       uint64_t seed, char* buf, int64_t cap) {
+    std::vector<int> xv(xs, xs + nx);
+    std::vector<double> pv(ps, ps + np);
+    const std::string t = sweep_band(size_t(length), xv, pv, seed);
+    const int64_t len = int64_t(t.size());
+    if (buf) std::memcpy(buf, t.data(), size_t(std::min(len, cap)));
+    return len;
 }
 
 }  // extern "C"

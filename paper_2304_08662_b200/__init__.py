@@ -9,6 +9,7 @@ from .xband import (BandBuffers, BandExceededError, DanglingReference, DevicePoo
                     ExtensionResult, ExtensionTask, InputError, OutOfRange, ScoringScheme,
                     SeedAlignment, SeedOutOfBounds, SeqView, Sequence, SequenceStore, SubMatrix,
                     UnknownSymbol, extend_batch, extend_seed, extend_tasks, extend_units, full,
-                    gcups, make_view, parse_submatrix, sim, split_lr, estimate_cost, xdrop_extend)
+                    gcups, make_view, parse_submatrix, sim, split_lr, estimate_cost, sweep_band,
+                    xdrop_extend)
 
 __all__ = ["capi", "synth", "xband"]

@@ -65,7 +65,8 @@ class XbStats(C.Structure):
                 ("ms_prep", C.c_double), ("ms_pilot", C.c_double), ("ms_tier", C.c_double * 6),
                 ("units_tier", C.c_int64 * 6), ("cells_tier", C.c_int64 * 6),
                 ("escalated", C.c_int64 * 6), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
-                ("sm_count", C.c_int32), ("start_tier", C.c_int32), ("dbg", C.c_int64 * 6)]
+                ("sm_count", C.c_int32), ("start_tier", C.c_int32), ("dbg", C.c_int64 * 6),
+                ("start_lane_groups", C.c_int32), ("reserved", C.c_int32)]
 
     def as_dict(self) -> dict:
         return {"n_devices": self.n_devices, "launches": self.launches,
@@ -74,7 +75,7 @@ class XbStats(C.Structure):
                 "cells_tier": list(self.cells_tier), "escalated": list(self.escalated),
                 "h2d_bytes": self.h2d_bytes, "d2h_bytes": self.d2h_bytes,
                 "sm_count": self.sm_count, "start_tier": self.start_tier,
-                "dbg": list(self.dbg)}
+                "dbg": list(self.dbg), "start_lane_groups": bool(self.start_lane_groups)}
 
 
 _lib = None
@@ -121,6 +122,8 @@ def lib() -> C.CDLL:
         "xb_synth_sizes": (V, [P, C.POINTER(I64)]),
         "xb_synth_copy": (V, [P, P, P, P]),
         "xb_synth_free": (V, [P]),
+        "xb_synth_pairs": (P, [C.c_uint64, C.c_uint64, C.c_double, I, I, C.c_uint64, C.POINTER(I)]),
+        "xb_sweep_band": (I, [C.c_uint64, P, C.c_int32, P, C.c_int32, C.c_uint64, P, C.POINTER(XbExec)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -138,7 +141,7 @@ EXPORTED = ["xb_version", "xb_strerror", "xb_device_count", "xb_scheme_match_mis
             "xb_extend_batch", "xb_extend_units", "xb_batch_create", "xb_batch_run",
             "xb_batch_sync", "xb_batch_fetch", "xb_batch_stats", "xb_batch_free",
             "xb_last_stats", "xb_measure_int32_peak", "xb_synth_make", "xb_synth_sizes",
-            "xb_synth_copy", "xb_synth_free"]
+            "xb_synth_copy", "xb_synth_free", "xb_synth_pairs", "xb_sweep_band"]
 
 
 class XbError(RuntimeError):

@@ -1311,6 +1311,7 @@ int xb_batch_stats(xb_batch* B, xb_stats* st) {
             st->escalated[t] += int64_t(c.escalated[t]);
         }
         st->start_tier = c.start_tier;
+        st->start_lane_groups = (D.n_units && D.all_group) ? 1 : 0;
         for (int q = 0; q < 6; ++q) st->dbg[q] += int64_t(c.dbg[q]);
         st->launches += D.launches;
         st->sm_count = D.sm_count;
@@ -1422,6 +1423,64 @@ int xb_extend_units(xb_pool* p, const xb_unit* units, int64_t n, int band, xb_si
     if (!rc) rc = xb_batch_stats(B, &g_last_stats);
     xb_batch_free(B);
     return rc;
+}
+
+int xb_sweep_band(uint64_t length, const int32_t* xs, int32_t nx, const double* ps, int32_t np,
+                  uint64_t rng_seed, int32_t* delta_w, const xb_exec* exec) {
+    if (nx < 0 || np < 0 || (nx && !xs) || (np && !ps) || (nx && np && !delta_w)) return XB_E_BAD_PARAM;
+    if (length + 1 > uint64_t(INT32_MAX)) return XB_E_BAD_PARAM;
+    for (int32_t a = 0; a < nx; ++a)
+        if (xs[a] < 0) return XB_E_BAD_PARAM;  // scoring.cpp:17-20
+    if (!nx || !np) return XB_OK;
+    // the np pairs (pipeline.cpp:188-195), shared by every X
+    std::vector<char> sym;
+    std::vector<int64_t> off{0};
+    for (int32_t b = 0; b < np; ++b) {
+        int err = 0;
+        xb_synth* S = xb_synth_pairs(1, length, ps[b], 17, 0, rng_seed, &err);
+        if (!S) return err;
+        int64_t z[6];
+        xb_synth_sizes(S, z);
+        const size_t base = sym.size();
+        sym.resize(base + size_t(z[1]));
+        std::vector<int64_t> o(size_t(z[0]) + 1);
+        xb_synth_copy(S, sym.data() + base, o.data(), nullptr);
+        xb_synth_free(S);
+        for (size_t q = 1; q < o.size(); ++q) off.push_back(int64_t(base) + o[q]);
+    }
+    // full views, both Right (pipeline.cpp:196-199); band = length + 1
+    std::vector<xb_unit> units(static_cast<size_t>(np));
+    for (int32_t b = 0; b < np; ++b)
+        units[size_t(b)] = xb_unit{uint32_t(2 * b), uint32_t(2 * b + 1), 1, 1, 0, 0, length, length};
+    std::vector<int> rcs(static_cast<size_t>(nx), XB_OK);
+    auto one_x = [&](int32_t a) {
+        int err = 0;
+        xb_scheme* sc = xb_scheme_match_mismatch(1, -1, -1, xs[a], &err);
+        if (!sc) {
+            rcs[size_t(a)] = err;
+            return;
+        }
+        xb_pool* pool = xb_pool_create(sc, &err);
+        xb_scheme_free(sc);
+        if (!pool) {
+            rcs[size_t(a)] = err;
+            return;
+        }
+        const int64_t id = xb_pool_add_bulk(pool, sym.data(), off.data(), int64_t(off.size()) - 1);
+        std::vector<xb_side_result> out(static_cast<size_t>(np));
+        int64_t bad = -1;
+        int rc = id < 0 ? int(-id) : xb_extend_units(pool, units.data(), np, int(length + 1), out.data(), &bad, exec);
+        for (int32_t b = 0; b < np && !rc; ++b) delta_w[size_t(a) * size_t(np) + size_t(b)] = out[size_t(b)].delta_w;
+        xb_pool_free(pool);
+        rcs[size_t(a)] = rc;
+    };
+    // the X values are independent batches: run them concurrently
+    std::vector<std::thread> th;
+    for (int32_t a = 0; a < nx; ++a) th.emplace_back(one_x, a);
+    for (auto& t : th) t.join();
+    for (int rc : rcs)
+        if (rc) return rc;
+    return XB_OK;
 }
 
 int xb_last_stats(xb_stats* st) {

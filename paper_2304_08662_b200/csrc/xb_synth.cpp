@@ -395,6 +395,48 @@ void make_overlap(xb_synth* S, double scale, uint64_t seed, int T) {
 
 }  // namespace
 
+namespace {
+
+// The reference's own pair generator (proj/src/io.cpp:198-255), restated:
+// H uniform over ACGT from raw mt19937_64 draws, V a copy whose non-seed
+// positions change to a strictly different base with probability 1 - p,
+// the seed at the centre (or uniform), h_seed = v_seed.  Raw engine draws
+// only, so every standard library gives the same bytes.
+int make_reference_pairs(xb_synth* S, uint64_t pairs, uint64_t length, double p_match, int k,
+                         int uniform, uint64_t seed) {
+    if (k < 1 || uint64_t(k) > length) return XB_E_BAD_PARAM;  // io.cpp:199-202 InputError
+    static const char kBases[4] = {'A', 'C', 'G', 'T'};
+    std::mt19937_64 rng(seed);
+    auto draw = [&]() -> uint64_t { return rng(); };
+    auto unit_interval = [&]() -> double { return double(draw() >> 11) * 0x1.0p-53; };
+    const bool never = p_match >= 1.0, always = p_match <= 0.0;
+    S->k = k;
+    S->symbols.reserve(size_t(2 * pairs * length));
+    for (uint64_t q = 0; q < pairs; ++q) {
+        std::string h(size_t(length), 'A');
+        for (uint64_t i = 0; i < length; ++i) h[size_t(i)] = kBases[draw() % 4];
+        uint64_t pos = (length - uint64_t(k)) / 2;
+        if (uniform) pos = draw() % (length - uint64_t(k) + 1);
+        std::string v = h;
+        for (uint64_t i = 0; i < length; ++i) {
+            if (i >= pos && i < pos + uint64_t(k)) continue;
+            if (never) continue;
+            if (!always && unit_interval() < p_match) continue;
+            int cur = 0;
+            while (kBases[cur] != v[size_t(i)]) ++cur;
+            v[size_t(i)] = kBases[(cur + 1 + int(draw() % 3)) % 4];
+        }
+        for (const std::string* x : {&h, &v}) {
+            S->symbols.insert(S->symbols.end(), x->begin(), x->end());
+            S->offsets.push_back(int64_t(S->symbols.size()));
+        }
+        S->tasks.insert(S->tasks.end(), {int64_t(2 * q), int64_t(2 * q + 1), int64_t(pos), int64_t(pos)});
+    }
+    return XB_OK;
+}
+
+}  // namespace
+
 extern "C" {
 
 xb_synth* xb_synth_make(int cfg, double scale, uint64_t seed, const char* matrix_text, int n_threads,
@@ -437,6 +479,19 @@ void xb_synth_copy(const xb_synth* s, char* symbols, int64_t* offsets, int64_t* 
     if (symbols) std::memcpy(symbols, s->symbols.data(), s->symbols.size());
     if (offsets) std::memcpy(offsets, s->offsets.data(), s->offsets.size() * 8);
     if (tasks) std::memcpy(tasks, s->tasks.data(), s->tasks.size() * 8);
+}
+
+xb_synth* xb_synth_pairs(uint64_t pairs, uint64_t length, double p_match, int k, int uniform_seed,
+                         uint64_t rng_seed, int* err) {
+    auto* S = new xb_synth();
+    const int rc = make_reference_pairs(S, pairs, length, p_match, k, uniform_seed, rng_seed);
+    if (rc) {
+        delete S;
+        if (err) *err = rc;
+        return nullptr;
+    }
+    if (err) *err = XB_OK;
+    return S;
 }
 
 void xb_synth_free(xb_synth* s) { delete s; }

@@ -68,3 +68,26 @@ def make(cfg: int, scale: float = 1.0, seed: int = 0, threads: int = 0) -> Datas
     finally:
         L.xb_synth_free(h)
     return Dataset(cfg, sym, off, tasks, k, x, band)
+
+
+def pairs(n_pairs: int, length: int, p_match: float, k: int = 17, seed: int = 42,
+          uniform_seed: bool = False):
+    """The reference's generate_synthetic (proj/src/io.cpp:198-255) through the
+    C ABI: (symbols uint8, offsets int64, tasks (n, 4) int64), byte-identical
+    to the reference for the same SynthParams."""
+    L = lib()
+    err = C.c_int(0)
+    h = L.xb_synth_pairs(n_pairs, length, p_match, k, int(uniform_seed), seed, C.byref(err))
+    from .xband import _raise  # the reference's InputError for k < 1 or k > length
+    _raise(err.value, "generate_synthetic")
+    try:
+        z = (C.c_int64 * 6)()
+        L.xb_synth_sizes(h, z)
+        n_seqs, total, n_tasks = int(z[0]), int(z[1]), int(z[2])
+        sym = np.empty(total, dtype=np.uint8)
+        off = np.empty(n_seqs + 1, dtype=np.int64)
+        tasks = np.empty((n_tasks, 4), dtype=np.int64)
+        L.xb_synth_copy(h, sym.ctypes.data, off.ctypes.data, tasks.ctypes.data)
+    finally:
+        L.xb_synth_free(h)
+    return sym, off, tasks

@@ -388,6 +388,26 @@ def extend_tasks(pool: DevicePool, tasks, k: int, band: int, exec_flags: int = 0
     return out, ss
 
 
+def sweep_band(length: int, xs, p_grid, rng_seed: int = 42, n_devices: int = 1,
+               device_ids=None) -> str:
+    """The band survey of proj/src/pipeline.cpp:181-208 (declared at
+    pipeline.hpp:58): for every X and p, one synthetic pair of `length`
+    (generate_synthetic, centred 17-mer seed) extended over the full views
+    with band length + 1; returns the reference's TSV byte for byte."""
+    xa = np.ascontiguousarray(list(xs), dtype=np.int32)
+    pa = np.ascontiguousarray(list(p_grid), dtype=np.float64)
+    dw = np.zeros(len(xa) * len(pa), dtype=np.int32)
+    ex = capi.make_exec(n_devices, device_ids, None, 0)
+    rc = lib().xb_sweep_band(length, xa.ctypes.data, len(xa), pa.ctypes.data, len(pa), rng_seed,
+                             dw.ctypes.data, C.byref(ex))
+    _raise(rc, "xb_sweep_band", -1)
+    rows = ["x\terror_rate\tdelta_w\n"]
+    for a, x in enumerate(xa):
+        for b, p in enumerate(pa):
+            rows.append("%d\t%.2f\t%d\n" % (int(x), 1.0 - float(p), int(dw[a * len(pa) + b])))
+    return "".join(rows)
+
+
 def last_stats() -> dict:
     st = capi.XbStats()
     lib().xb_last_stats(C.byref(st))

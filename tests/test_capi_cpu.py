@@ -116,3 +116,27 @@ def test_split_lr_mirror():
     with pytest.raises(xb.SeedOutOfBounds):
         xb.split_lr(xb.ExtensionTask(0, 0, 1, 90, 0), store, 17)
     assert xb.gcups(1000, 1000, 1e-3) == pytest.approx(1.0)
+
+
+def test_synth_pairs_match_reference_generator():
+    """xb_synth_pairs restates generate_synthetic (io.cpp:198-255): same bytes,
+    offsets and seed tasks as the reference's own generator."""
+    import hashlib
+    g = load_json("sweep_band.json")
+    for c in g["synth"]:
+        sym, off, tasks = synth.pairs(c["pairs"], c["length"], c["p_match"], c["k"], c["seed"],
+                                      c["uniform_seed"])
+        assert hashlib.sha256(sym.tobytes()).hexdigest() == c["symbols_sha256"], c
+        assert off.tolist() == c["offsets"] and tasks.tolist() == c["tasks"], c
+    with pytest.raises(xb.InputError):
+        synth.pairs(1, 10, 0.9, 17)  # k > length (io.cpp:200-202)
+    with pytest.raises(xb.InputError):
+        synth.pairs(1, 10, 0.9, 0)
+
+
+def test_sweep_band_validation_precedes_device():
+    with pytest.raises(xb.InputError):
+        xb.sweep_band(100, [-1], [0.9])  # X < 0 (scoring.cpp:17-20)
+    with pytest.raises(xb.InputError):
+        xb.sweep_band(10, [5], [0.9])  # 17-mer seed longer than the pair
+    assert xb.sweep_band(100, [], [0.9]) == "x\terror_rate\tdelta_w\n"

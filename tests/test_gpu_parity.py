@@ -291,3 +291,12 @@ def test_multi_device_sharding_same_results(xb):
     assert result_rows_equal(a, b).all() and (sa == sb).all()
     st = xb.xband.last_stats()
     assert st["n_devices"] == 2
+
+
+def test_sweep_band_matches_reference(xb):
+    """§8(f) band survey on the GPU (pipeline.cpp:181-208): the reference's TSV
+    byte for byte, including acceptance criterion 2 (L=20000, p=0.9, X=15:
+    spread 20) and criterion 3's grid, and the paper-scale grid."""
+    g = load_json("sweep_band.json")
+    for c in g["sweeps"]:
+        assert xb.sweep_band(c["length"], c["xs"], c["ps"], c["seed"]) == c["tsv"], c["source"]
