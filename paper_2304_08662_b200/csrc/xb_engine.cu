@@ -258,7 +258,6 @@ struct xb_pool {
     std::vector<int64_t> seq_pos, seq_len;
     DevScheme dev_scheme{};
     std::map<int, DevPool> dev;
-    std::map<int, std::vector<Workspace*>> ws;  // reusable per-device batch buffers
     std::mutex mu;
 };
 
@@ -391,7 +390,6 @@ static void pool_drop_devices(xb_pool* p) {
     p->dev.clear();
 }
 
-static void destroy_workspaces(xb_pool* p);
 
 extern "C" {
 
@@ -461,7 +459,6 @@ void xb_pool_evict(xb_pool* p) {
 
 void xb_pool_free(xb_pool* p) {
     if (!p) return;
-    destroy_workspaces(p);
     pool_drop_devices(p);
     if (p->host_words) cudaFreeHost(p->host_words);
     delete p;
@@ -560,14 +557,6 @@ struct Workspace {
     }
 };
 
-static void destroy_workspaces(xb_pool* p) {
-    for (auto& kv : p->ws)
-        for (Workspace* w : kv.second) {
-            w->destroy();
-            delete w;
-        }
-    p->ws.clear();
-}
 
 struct DevBatch {
     int dev = 0;
@@ -584,7 +573,6 @@ struct DevBatch {
     TierParams tp{};           // planned launch parameters (run_plan -> run_cascade)
     bool all_group = false, no_group = false;
     Workspace* ws = nullptr;
-    bool ws_cached = false;
     DevPool* pool = nullptr;
     std::vector<int64_t> tasks;  // global task (or unit) indices of this shard
     int64_t n_items = 0;         // tasks (or units) on this device
@@ -626,16 +614,42 @@ struct xb_batch {
     bool ran = false;
 };
 
-static void free_dev(xb_pool* p, DevBatch& D) {
+// Batch workspaces hold no pool data, so they are reused across calls and
+// pools: a process-wide idle list per device, bounded in count and bytes.
+// (Never destroyed at exit: the CUDA runtime may already be gone then.)
+struct WorkspaceCache {
+    std::mutex mu;
+    std::map<int, std::vector<Workspace*>> idle;
+};
+static WorkspaceCache& ws_cache() {
+    static WorkspaceCache* c = new WorkspaceCache();
+    return *c;
+}
+constexpr size_t kIdleWorkspaces = 16;
+constexpr int64_t kIdleBytes = 8LL << 30;
+
+static int64_t ws_bytes(const Workspace* w) {
+    return w->capU * 160 + w->capI * 40 + int64_t(w->scratch_bytes) + int64_t(kResumeCap) * kResumeStride * 4;
+}
+
+static void free_dev(xb_pool*, DevBatch& D) {
     if (!D.ws) return;
-    if (D.ws_cached) {
-        std::lock_guard<std::mutex> g(p->mu);
-        D.ws->in_use = false;
-    } else {
-        D.ws->destroy();
-        delete D.ws;
-    }
+    Workspace* w = D.ws;
     D.ws = nullptr;
+    WorkspaceCache& c = ws_cache();
+    {
+        std::lock_guard<std::mutex> g(c.mu);
+        auto& v = c.idle[w->dev];
+        int64_t held = 0;
+        for (Workspace* x : v) held += ws_bytes(x);
+        if (v.size() < kIdleWorkspaces && held + ws_bytes(w) <= kIdleBytes) {
+            w->in_use = false;
+            v.push_back(w);
+            return;
+        }
+    }
+    w->destroy();
+    delete w;
 }
 
 // longest-first estimate for a unit, shared with the prep kernel
@@ -645,30 +659,25 @@ static inline long long unit_est(long long hl, long long vl) {
     return 2 * mn + std::min(gd, 64LL);
 }
 
-static Workspace* acquire_workspace(xb_pool* p, int dev, bool* cached) {
-    std::lock_guard<std::mutex> g(p->mu);
-    auto& v = p->ws[dev];
-    for (Workspace* w : v)
-        if (!w->in_use) {
-            w->in_use = true;
-            *cached = true;
-            return w;
-        }
+static Workspace* acquire_workspace(int dev) {
+    WorkspaceCache& c = ws_cache();
+    std::lock_guard<std::mutex> g(c.mu);
+    auto& v = c.idle[dev];
+    if (!v.empty()) {
+        Workspace* w = v.back();  // most recently used: its buffers are likely big enough
+        v.pop_back();
+        w->in_use = true;
+        return w;
+    }
     auto* w = new Workspace();
     w->dev = dev;
     w->in_use = true;
-    if (v.size() < 2) {  // keep a couple per device; extra concurrent batches are transient
-        v.push_back(w);
-        *cached = true;
-    } else {
-        *cached = false;
-    }
     return w;
 }
 
 static int setup_device(xb_batch* B, DevBatch& D, const xb_exec* ex) {
     CK(cudaSetDevice(D.dev));
-    D.ws = acquire_workspace(B->pool, D.dev, &D.ws_cached);
+    D.ws = acquire_workspace(D.dev);
     Workspace& W = *D.ws;
     if (!W.stream) {
         CK(cudaStreamCreateWithFlags(&W.stream, cudaStreamNonBlocking));
@@ -717,7 +726,9 @@ static int setup_device(xb_batch* B, DevBatch& D, const xb_exec* ex) {
     // warp-tier scratch: 2*band ints per resident warp, capped at 1 GiB
     {
         const int64_t per_warp = 2LL * B->band * 4;
-        int64_t warps = int64_t(D.sm_count) * 16;
+        // one warp slot per unit at most: a small batch with a huge band (the
+        // band survey: band = L + 1) needs kilobytes, not the full 16 per SM
+        int64_t warps = std::min<int64_t>(int64_t(D.sm_count) * 16, std::max<int64_t>(D.n_units, 4));
         warps = std::min<int64_t>(warps, std::max<int64_t>(4, (1LL << 30) / per_warp));
         warps = (warps + 3) / 4 * 4;
         D.scratch_warps = int(warps);

@@ -19,7 +19,7 @@ GRIDS = {
 R = Ref()
 out = {}
 for name, (L, xs, ps) in GRIDS.items():
-    xb.sweep_band(L, xs[:1], ps[:1])  # warm-up (context, workspaces)
+    xb.sweep_band(L, xs, ps)  # warm-up: context, one cached workspace per concurrent X
     t0 = time.perf_counter()
     g = xb.sweep_band(L, xs, ps)
     tg = time.perf_counter() - t0
@@ -29,4 +29,5 @@ for name, (L, xs, ps) in GRIDS.items():
     out[name] = {"length": L, "n_x": len(xs), "n_p": len(ps), "cells_grid": len(xs) * len(ps),
                  "gpu_s": tg, "reference_cpu_s": tr, "speedup": tr / tg, "identical_tsv": g == r}
     print(name, json.dumps(out[name]), flush=True)
-json.dump(out, open(os.path.join(ROOT, "profiles", "r1_sweep_band.json"), "w"), indent=1)
+dst = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "profiles", "r1_sweep_band.json")
+json.dump(out, open(dst, "w"), indent=1)
