@@ -9,7 +9,7 @@ LIB := paper_2304_08662_b200/_lib/libxdrop_b200.so
 OBJDIR := build
 
 SRCS_CU := $(CSRC)/xb_kernels.cu $(CSRC)/xb_thread.cu $(CSRC)/xb_group.cu $(CSRC)/xb_engine.cu
-SRCS_CPP := $(CSRC)/xb_synth.cpp
+SRCS_CPP := $(CSRC)/xb_synth.cpp $(CSRC)/xb_ingest.cpp
 HDRS := $(CSRC)/xb_internal.h $(CSRC)/xb_kernels.cuh include/xdrop_b200.h
 
 all: lib oracle
@@ -38,7 +38,11 @@ $(OBJDIR)/xb_synth.o: $(CSRC)/xb_synth.cpp include/xdrop_b200.h
 	@mkdir -p $(OBJDIR)
 	/usr/bin/g++ -O3 -std=c++17 -fPIC -c -o $@ $<
 
-$(LIB): $(OBJDIR)/xb_kernels.o $(OBJDIR)/xb_thread.o $(OBJDIR)/xb_group.o $(OBJDIR)/xb_engine.o $(OBJDIR)/xb_synth.o
+$(OBJDIR)/xb_ingest.o: $(CSRC)/xb_ingest.cpp include/xdrop_b200.h
+	@mkdir -p $(OBJDIR)
+	/usr/bin/g++ -O3 -std=c++17 -fPIC -Wall -c -o $@ $<
+
+$(LIB): $(OBJDIR)/xb_kernels.o $(OBJDIR)/xb_thread.o $(OBJDIR)/xb_group.o $(OBJDIR)/xb_engine.o $(OBJDIR)/xb_synth.o $(OBJDIR)/xb_ingest.o
 	@mkdir -p $(dir $(LIB))
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^ -lpthread
 

@@ -198,6 +198,48 @@ void xb_synth_free(xb_synth* s);
 xb_synth* xb_synth_pairs(uint64_t pairs, uint64_t length, double p_match, int k, int uniform_seed,
                          uint64_t rng_seed, int* err);
 
+/* ---- ingest of the reference's input formats (proj/src/io.cpp:58-196) ---- */
+/* Parse errors carry the reference's exception kind (errors.hpp:54-82), the
+ * 1-based line where the exception has one (InvalidSymbol, MalformedLine;
+ * else 0, the line is then in the text) and its what() text. */
+#define XB_PARSE_OK 0
+#define XB_PARSE_MISSING_HEADER 1   /* MissingHeader */
+#define XB_PARSE_EMPTY_RECORD 2     /* EmptyRecord */
+#define XB_PARSE_INVALID_SYMBOL 3   /* InvalidSymbol (line) */
+#define XB_PARSE_MALFORMED_LINE 4   /* MalformedLine (line) */
+#define XB_PARSE_NEGATIVE_INDEX 5   /* NegativeIndex */
+#define XB_PARSE_BAD_HEADER 6       /* BadHeader */
+#define XB_PARSE_OUT_OF_SHAPE 7     /* IndexOutOfDeclaredShape */
+#define XB_PARSE_BAD_ARGUMENT 8     /* null text / negative length (no reference analogue) */
+typedef struct {
+    int32_t kind;
+    int32_t reserved;
+    int64_t line;
+    char message[256];
+} xb_parse_error;
+
+/* parse_fasta (io.cpp:58-96): records of `text` (LF or CRLF), symbols
+ * upper-cased and checked against `allowed`, into one contiguous buffer on
+ * all host threads (n_threads <= 0: all).  NULL on a parse error (*err). */
+typedef struct xb_fasta xb_fasta;
+xb_fasta* xb_fasta_parse(const char* text, int64_t len, const char* allowed, int n_threads,
+                         xb_parse_error* err);
+/* sizes: [0] records, [1] symbol bytes, [2] name bytes */
+void xb_fasta_sizes(const xb_fasta* f, int64_t* sizes3);
+/* symbols; offsets (records+1); names concatenated; name_offsets (records+1) */
+void xb_fasta_copy(const xb_fasta* f, char* symbols, int64_t* offsets, char* names,
+                   int64_t* name_offsets);
+/* appends every record to the pool (ids in file order, as xb_pool_add_bulk) */
+int64_t xb_pool_add_fasta(xb_pool* p, const xb_fasta* f);
+void xb_fasta_free(xb_fasta* f);
+/* parse_seeds (io.cpp:98-127) / parse_overlaps (io.cpp:129-196, Matrix
+ * Market coordinate pattern|integer general, 1-based ids): tasks in input
+ * order, task_id = ordinal.  Returns the task count (at most `cap` written;
+ * call with cap 0 to size), or -XB_E_PARSE with *err filled. */
+int64_t xb_parse_seeds(const char* text, int64_t len, xb_task* out, int64_t cap, xb_parse_error* err);
+int64_t xb_parse_overlaps(const char* text, int64_t len, xb_task* out, int64_t cap,
+                          xb_parse_error* err);
+
 /* ---- band survey (sweep_band, proj/src/pipeline.cpp:181-208) ---- */
 /* For every X in xs and every p in ps: one synthetic pair (xb_synth_pairs
  * with pairs = 1, k = 17, centred seed, rng_seed), extended over the full

@@ -250,6 +250,42 @@ class Ref:
                                         int(uniform_seed), buf, cap, C.byref(ec))
         return ec.value, buf.raw[:n].decode()
 
+    def parse_fasta(self, text: bytes, allowed: str = "ACGTN"):
+        """The reference's parse_fasta: (symbols bytes, offsets, names) or
+        ("error", kind, line, message) with kind as XB_PARSE_*."""
+        n = len(text)
+        nrec = text.count(b">") + 2  # records <= headers
+        sym = C.create_string_buffer(n + 1)
+        off = np.zeros(nrec, dtype=np.int64)
+        names = C.create_string_buffer(n + 1)
+        noff = np.zeros(nrec, dtype=np.int64)
+        kind, line, msg = C.c_int(0), C.c_int64(0), C.create_string_buffer(256)
+        f = self.lib.ref_parse_fasta
+        f.restype = C.c_int64
+        f.argtypes = [C.c_char_p, C.c_int64, C.c_char_p] + [C.c_void_p] * 4 + [C.c_void_p] * 3
+        r = f(text, n, allowed.encode(), sym, off.ctypes.data, names, noff.ctypes.data,
+              C.byref(kind), C.byref(line), msg)
+        if r < 0:
+            return ("error", kind.value, line.value, msg.value.decode())
+        r = int(r)
+        raw = names.raw  # one copy (every .raw access copies the whole buffer)
+        return (sym.raw[: off[r]], off[: r + 1].copy(),
+                [raw[noff[i]:noff[i + 1]].decode() for i in range(r)])
+
+    def parse_tasks(self, text: bytes, overlaps: bool):
+        """The reference's parse_seeds / parse_overlaps: (n, 5) int64
+        (task_id, h, v, h_seed, v_seed) or ("error", kind, line, message)."""
+        cap = text.count(b"\n") + 2  # tasks <= lines
+        tasks = np.zeros((cap, 5), dtype=np.int64)
+        kind, line, msg = C.c_int(0), C.c_int64(0), C.create_string_buffer(256)
+        f = self.lib.ref_parse_tasks
+        f.restype = C.c_int64
+        f.argtypes = [C.c_int, C.c_char_p, C.c_int64, C.c_void_p, C.c_int64] + [C.c_void_p] * 3
+        r = f(int(overlaps), text, len(text), tasks.ctypes.data, cap, C.byref(kind), C.byref(line), msg)
+        if r < 0:
+            return ("error", kind.value, line.value, msg.value.decode())
+        return tasks[: int(r)].copy()
+
     def sweep_band(self, length, xs, ps, seed=42) -> str:
         """The reference's band survey TSV (pipeline.cpp:181-208)."""
         xa = np.ascontiguousarray(xs, dtype=np.int32)

@@ -23,6 +23,8 @@
 #include <vector>
 
 #include "xband/align.hpp"
+#include "xband/errors.hpp"
+#include "xband/io.hpp"
 #include "xband/partition.hpp"
 #include "xband/pipeline.hpp"
 #include "xband/scoring.hpp"
@@ -297,6 +299,75 @@ int64_t ref_sweep_band(int64_t length, const int* xs, int nx, const double* ps, 
     const int64_t len = int64_t(t.size());
     if (buf) std::memcpy(buf, t.data(), size_t(std::min(len, cap)));
     return len;
+}
+
+/* the reference's parsers (io.cpp:58-196), for the ingest parity tests:
+ * kind codes as XB_PARSE_* in include/xdrop_b200.h */
+static int parse_kind(const std::exception& e, int64_t* line) {
+    *line = 0;
+    if (auto* x = dynamic_cast<const InvalidSymbol*>(&e)) { *line = int64_t(x->line); return 3; }
+    if (auto* x = dynamic_cast<const MalformedLine*>(&e)) { *line = int64_t(x->line); return 4; }
+    if (dynamic_cast<const MissingHeader*>(&e)) return 1;
+    if (dynamic_cast<const EmptyRecord*>(&e)) return 2;
+    if (dynamic_cast<const NegativeIndex*>(&e)) return 5;
+    if (dynamic_cast<const BadHeader*>(&e)) return 6;
+    if (dynamic_cast<const IndexOutOfDeclaredShape*>(&e)) return 7;
+    return 99;
+}
+
+static void put_msg(const std::exception& e, char* msg, int64_t cap) {
+    const std::string m = e.what();
+    const size_t n = std::min<size_t>(m.size(), size_t(cap) - 1);
+    std::memcpy(msg, m.data(), n);
+    msg[n] = 0;
+}
+
+/* returns records (sym/off/names/name_off filled; buffers sized by the
+ * caller from len) or -1 with kind/line/msg */
+int64_t ref_parse_fasta(const char* text, int64_t len, const char* allowed, char* sym, int64_t* off,
+                        char* names, int64_t* name_off, int* kind, int64_t* line, char* msg) {
+    try {
+        SequenceStore st = parse_fasta(std::string(text, size_t(len)), std::string(allowed));
+        int64_t a = 0, b = 0;
+        off[0] = 0;
+        name_off[0] = 0;
+        for (size_t i = 0; i < st.size(); ++i) {
+            std::memcpy(sym + a, st[i].symbols.data(), st[i].symbols.size());
+            a += int64_t(st[i].symbols.size());
+            off[i + 1] = a;
+            std::memcpy(names + b, st[i].name.data(), st[i].name.size());
+            b += int64_t(st[i].name.size());
+            name_off[i + 1] = b;
+        }
+        *kind = 0;
+        return int64_t(st.size());
+    } catch (const std::exception& e) {
+        *kind = parse_kind(e, line);
+        put_msg(e, msg, 256);
+        return -1;
+    }
+}
+
+/* which = 0 seeds, 1 overlaps; tasks: 5 int64 per task (task_id, h, v, hs, vs) */
+int64_t ref_parse_tasks(int which, const char* text, int64_t len, int64_t* tasks, int64_t cap,
+                        int* kind, int64_t* line, char* msg) {
+    try {
+        const std::string t(text, size_t(len));
+        std::vector<ExtensionTask> v = which ? parse_overlaps(t) : parse_seeds(t);
+        for (size_t i = 0; i < v.size() && int64_t(i) < cap; ++i) {
+            tasks[5 * i + 0] = v[i].task_id;
+            tasks[5 * i + 1] = v[i].h_id;
+            tasks[5 * i + 2] = v[i].v_id;
+            tasks[5 * i + 3] = int64_t(v[i].h_seed);
+            tasks[5 * i + 4] = int64_t(v[i].v_seed);
+        }
+        *kind = 0;
+        return int64_t(v.size());
+    } catch (const std::exception& e) {
+        *kind = parse_kind(e, line);
+        put_msg(e, msg, 256);
+        return -1;
+    }
 }
 
 }  // extern "C"

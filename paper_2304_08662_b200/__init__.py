@@ -10,6 +10,8 @@ from .xband import (BandBuffers, BandExceededError, DanglingReference, DevicePoo
                     SeedAlignment, SeedOutOfBounds, SeqView, Sequence, SequenceStore, SubMatrix,
                     UnknownSymbol, extend_batch, extend_seed, extend_tasks, extend_units, full,
                     gcups, make_view, parse_submatrix, sim, split_lr, estimate_cost, sweep_band,
-                    xdrop_extend)
+                    xdrop_extend, parse_fasta, parse_seeds, parse_overlaps, FastaRecords,
+                    MissingHeader, EmptyRecord, InvalidSymbol, MalformedLine, NegativeIndex,
+                    BadHeader, IndexOutOfDeclaredShape)
 
 __all__ = ["capi", "synth", "xband"]

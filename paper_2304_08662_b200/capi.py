@@ -122,6 +122,13 @@ def lib() -> C.CDLL:
         "xb_synth_sizes": (V, [P, C.POINTER(I64)]),
         "xb_synth_copy": (V, [P, P, P, P]),
         "xb_synth_free": (V, [P]),
+        "xb_fasta_parse": (P, [P, I64, C.c_char_p, I, P]),
+        "xb_fasta_sizes": (V, [P, P]),
+        "xb_fasta_copy": (V, [P, P, P, P, P]),
+        "xb_pool_add_fasta": (I64, [P, P]),
+        "xb_fasta_free": (V, [P]),
+        "xb_parse_seeds": (I64, [P, I64, P, I64, P]),
+        "xb_parse_overlaps": (I64, [P, I64, P, I64, P]),
         "xb_synth_pairs": (P, [C.c_uint64, C.c_uint64, C.c_double, I, I, C.c_uint64, C.POINTER(I)]),
         "xb_sweep_band": (I, [C.c_uint64, P, C.c_int32, P, C.c_int32, C.c_uint64, P, C.POINTER(XbExec)]),
     }
@@ -141,7 +148,18 @@ EXPORTED = ["xb_version", "xb_strerror", "xb_device_count", "xb_scheme_match_mis
             "xb_extend_batch", "xb_extend_units", "xb_batch_create", "xb_batch_run",
             "xb_batch_sync", "xb_batch_fetch", "xb_batch_stats", "xb_batch_free",
             "xb_last_stats", "xb_measure_int32_peak", "xb_synth_make", "xb_synth_sizes",
-            "xb_synth_copy", "xb_synth_free", "xb_synth_pairs", "xb_sweep_band"]
+            "xb_synth_copy", "xb_synth_free", "xb_synth_pairs", "xb_sweep_band", "xb_fasta_parse",
+            "xb_fasta_sizes", "xb_fasta_copy", "xb_pool_add_fasta", "xb_fasta_free", "xb_parse_seeds",
+            "xb_parse_overlaps"]
+
+
+class XbParseError(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("reserved", C.c_int32), ("line", C.c_int64),
+                ("message", C.c_char * 256)]
+
+
+XB_PARSE_NAMES = ["ok", "MissingHeader", "EmptyRecord", "InvalidSymbol", "MalformedLine",
+                  "NegativeIndex", "BadHeader", "IndexOutOfDeclaredShape", "BadArgument"]
 
 
 class XbError(RuntimeError):

@@ -64,6 +64,59 @@ class DeviceError(InternalError):
     pass
 
 
+# parser errors (errors.hpp:54-82), each naming the offending line where the
+# reference does
+class MissingHeader(InputError):
+    pass
+
+
+class EmptyRecord(InputError):
+    pass
+
+
+class InvalidSymbol(InputError):
+    def __init__(self, line: int, msg: str):
+        super().__init__(msg)
+        self.line = line
+
+
+class MalformedLine(InputError):
+    def __init__(self, line: int, msg: str):
+        super().__init__(msg)
+        self.line = line
+
+
+class NegativeIndex(InputError):
+    pass
+
+
+class BadHeader(InputError):
+    pass
+
+
+class IndexOutOfDeclaredShape(InputError):
+    pass
+
+
+def _raise_parse(e) -> None:
+    msg = e.message.decode()
+    if e.kind == 1:
+        raise MissingHeader(msg)
+    if e.kind == 2:
+        raise EmptyRecord(msg)
+    if e.kind == 3:
+        raise InvalidSymbol(int(e.line), msg)
+    if e.kind == 4:
+        raise MalformedLine(int(e.line), msg)
+    if e.kind == 5:
+        raise NegativeIndex(msg)
+    if e.kind == 6:
+        raise BadHeader(msg)
+    if e.kind == 7:
+        raise IndexOutOfDeclaredShape(msg)
+    raise InputError(msg or "invalid argument")
+
+
 class BandExceededError(RuntimeError):
     """Retry signal (errors.hpp:80-93): the live spread outgrew the band."""
 
@@ -228,6 +281,19 @@ class DevicePool:
         self.n = n
 
     @staticmethod
+    def from_fasta(text_or_records, scheme: ScoringScheme, allowed: str = "ACGTN") -> "DevicePool":
+        """FASTA text (or FastaRecords) straight into a packed pool: records in
+        file order are sequence ids 0..n-1 (parse_fasta + SequenceStore)."""
+        rec = text_or_records if isinstance(text_or_records, FastaRecords) else \
+            FastaRecords(text_or_records, allowed)
+        p = DevicePool(scheme, b"", np.zeros(1, dtype=np.int64))
+        r = lib().xb_pool_add_fasta(p._h, rec._h)
+        if r < 0:
+            _raise(int(-r), "xb_pool_add_fasta")
+        p.n = len(rec)
+        return p
+
+    @staticmethod
     def from_store(store, scheme: ScoringScheme) -> "DevicePool":
         data = b"".join(s.symbols.encode() for s in store)
         off = np.zeros(len(store) + 1, dtype=np.int64)
@@ -386,6 +452,79 @@ def extend_tasks(pool: DevicePool, tasks, k: int, band: int, exec_flags: int = 0
                                ss.ctypes.data, C.byref(bad), C.byref(ex))
     _raise(rc, "xb_extend_batch", bad.value)
     return out, ss
+
+
+# ---------------------------------------------------------------- ingest ----
+# proj/src/io.cpp:58-196, native (csrc/xb_ingest.cpp)
+
+def _text(t) -> bytes:
+    return t.encode() if isinstance(t, str) else bytes(t)
+
+
+class FastaRecords:
+    """parse_fasta output as contiguous buffers: symbols (uint8), offsets,
+    names; `handle` can feed a DevicePool without another copy."""
+
+    def __init__(self, text, allowed: str = "ACGTN", threads: int = 0):
+        b = _text(text)
+        err = capi.XbParseError()
+        self._h = lib().xb_fasta_parse(b, len(b), allowed.encode(), threads, C.byref(err))
+        if not self._h:
+            _raise_parse(err)
+        z = (C.c_int64 * 3)()
+        lib().xb_fasta_sizes(self._h, z)
+        n, ns, nb = int(z[0]), int(z[1]), int(z[2])
+        self.symbols = np.empty(ns, dtype=np.uint8)
+        self.offsets = np.empty(n + 1, dtype=np.int64)
+        names = np.empty(nb, dtype=np.uint8)
+        noff = np.empty(n + 1, dtype=np.int64)
+        lib().xb_fasta_copy(self._h, self.symbols.ctypes.data, self.offsets.ctypes.data,
+                            names.ctypes.data, noff.ctypes.data)
+        nbytes = names.tobytes()
+        self.names = [nbytes[noff[i]:noff[i + 1]].decode() for i in range(n)]
+
+    def __len__(self):
+        return len(self.names)
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib().xb_fasta_free(self._h)
+        except Exception:
+            pass
+
+
+def parse_fasta(text, allowed: str = "ACGTN") -> SequenceStore:
+    """parse_fasta (io.cpp:58-96): records with upper-cased symbols checked
+    against `allowed`; MissingHeader / EmptyRecord / InvalidSymbol as there."""
+    r = FastaRecords(text, allowed)
+    st = SequenceStore()
+    sym = r.symbols.tobytes()
+    for i, name in enumerate(r.names):
+        st.append(Sequence(i, name, sym[r.offsets[i]:r.offsets[i + 1]].decode()))
+    return st
+
+
+def _parse_tasks(fn, text) -> np.ndarray:
+    b = _text(text)
+    err = capi.XbParseError()
+    n = fn(b, len(b), None, 0, C.byref(err))
+    if n < 0:
+        _raise_parse(err)
+    out = np.zeros(int(n), dtype=TASK_DTYPE)
+    if n:
+        fn(b, len(b), out.ctypes.data, int(n), C.byref(err))
+    return out
+
+
+def parse_seeds(text) -> np.ndarray:
+    """parse_seeds (io.cpp:98-127): TASK_DTYPE rows in input order."""
+    return _parse_tasks(lib().xb_parse_seeds, text)
+
+
+def parse_overlaps(text) -> np.ndarray:
+    """parse_overlaps (io.cpp:129-196): Matrix Market coordinate overlaps."""
+    return _parse_tasks(lib().xb_parse_overlaps, text)
 
 
 def sweep_band(length: int, xs, p_grid, rng_seed: int = 42, n_devices: int = 1,
