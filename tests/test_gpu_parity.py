@@ -300,3 +300,60 @@ def test_sweep_band_matches_reference(xb):
     g = load_json("sweep_band.json")
     for c in g["sweeps"]:
         assert xb.sweep_band(c["length"], c["xs"], c["ps"], c["seed"]) == c["tsv"], c["source"]
+
+
+def test_route_guard_mixed_batch(xb, oracle):
+    """Units whose drift-space values could pass 2^23 (host/prep bound:
+    max_score*min(n,m) + beta*(n+m+2) + X) go to the warp tier, the rest to
+    the thread tiers, in one batch, both exact.  The bound is set by the view
+    lengths (scheme +1/-2/-2: bound = min(n,m) + 2(n+m+2) + X + 2): 3M-base
+    views route to the warp tier, 1.5M-base and short ones do not.  A
+    ~1000-base shared prefix, then unrelated sequence (negative drift under
+    this scheme) keeps every X-drop short."""
+    rng = np.random.default_rng(23)
+    acgt = np.frombuffer(b"ACGT", dtype=np.uint8)
+    entries = []
+    for n in (3_000_000, 1_500_000, 700, 3_000_001, 150):
+        pre = int(min(n, 1000))
+        h = rng.choice(acgt, n)
+        v = rng.choice(acgt, n)
+        v[:pre] = h[:pre]
+        mut = rng.random(pre) < 0.05
+        v[:pre][mut] = rng.choice(acgt, int(mut.sum()))
+        entries.append((h.tobytes(), v.tobytes()))
+    sym = b"".join(h + v for h, v in entries)
+    off = [0]
+    for h, v in entries:
+        off += [off[-1] + len(h), off[-1] + len(h) + len(v)]
+    from paper_2304_08662_b200.capi import UNIT_DTYPE
+    units = np.zeros(len(entries), dtype=UNIT_DTYPE)
+    for q, (h, v) in enumerate(entries):
+        units[q] = (2 * q, 2 * q + 1, 1, 1, 0, 0, len(h), len(v))
+    band = 256
+    pool = xb.DevicePool(xb.ScoringScheme.match_mismatch(1, -2, -2, 10), sym, np.array(off))
+    out = xb.extend_units(pool, units, band)
+    st = xb.xband.last_stats()
+    assert st["units_tier"][5] == 2 and sum(st["units_tier"][:5]) == 3, st["units_tier"]
+    assert sum(st["escalated"]) == 0, st["escalated"]
+    so = oracle.scheme_mm(1, -2, -2, 10)
+    for q, (h, v) in enumerate(entries):
+        assert rec_tuple(out[q]) == rec_tuple(oracle.extend(h, v, so, band)), q
+
+
+def test_million_base_self_extension_both_directions(xb):
+    """Maximum-size views: a 1,048,579-base read against itself from a seed in
+    the middle, left (reversing view) and right, plus a 3-base mismatch tail."""
+    rng = np.random.default_rng(5)
+    n = (1 << 20) + 3
+    s = rng.choice(np.frombuffer(b"ACGT", dtype=np.uint8), n).tobytes()
+    t = s[:-3] + bytes((b"ACGT"[(b"ACGT".index(c) + 1) % 4] for c in s[-3:]))
+    pool = xb.DevicePool(xb.ScoringScheme.match_mismatch(1, -1, -1, 10), s + t,
+                         np.array([0, n, 2 * n], dtype=np.int64))
+    seed = n // 2 - 7
+    out, ss = xb.extend_tasks(pool, np.array([[0, 1, seed, seed]]), 17, 64)
+    L, R = out[0], out[1]
+    assert ss[0] == 17
+    assert (L["score"], L["h_ext"], L["v_ext"]) == (seed, seed, seed)
+    right = n - seed - 17
+    assert (R["score"], R["h_ext"], R["v_ext"]) == (right - 3, right - 3, right - 3)
+    assert L["status"] == 0 and R["status"] == 0
