@@ -357,3 +357,33 @@ def test_million_base_self_extension_both_directions(xb):
     right = n - seed - 17
     assert (R["score"], R["h_ext"], R["v_ext"]) == (right - 3, right - 3, right - 3)
     assert L["status"] == 0 and R["status"] == 0
+
+
+@pytest.mark.parametrize("case", ["dna_table_2bit", "protein_bytes"])
+def test_table_modes_at_throughput_scale(xb, oracle, case):
+    """The table modes (2-bit pool with a non-unit DNA scheme; byte pool with
+    BLOSUM62) through the thread tiers at batch scale (throughput planning:
+    pilot, K24 threads, resumed escalations, streamed byte windows, sentinel
+    bytes at view ends), a seeded sample checked against the oracle."""
+    from paper_2304_08662_b200 import synth
+    if case == "dna_table_2bit":
+        ds = synth.make(2, 0.2)
+        s = xb.ScoringScheme.match_mismatch(2, -3, -5, 40)
+        so = oracle.scheme_mm(2, -3, -5, 40)
+    else:
+        ds = synth.make(3, 1.0)
+        s = xb.ScoringScheme.from_matrix(xb.parse_submatrix(synth.blosum62_text()), -1, ds.x)
+        so = oracle_scheme(oracle, ["BLOSUM62", -1, ds.x])
+    pool = xb.DevicePool(s, ds.symbols, ds.offsets)
+    assert pool.bits_per_symbol == (2 if case == "dna_table_2bit" else 8)
+    out, ss = xb.extend_tasks(pool, ds.tasks, ds.k, ds.band, exec_flags=128 | 64)  # THROUGHPUT, threads
+    st = xb.xband.last_stats()
+    assert not st["start_lane_groups"]
+    rng = np.random.default_rng(7)
+    pick = np.sort(rng.choice(ds.n_tasks, size=min(ds.n_tasks, 250), replace=False))
+    exp, ess = oracle.extend_batch(ds.symbols, ds.offsets, ds.tasks[pick], ds.k, so, ds.band,
+                                   threads=os.cpu_count() or 1)
+    assert result_rows_equal(out.reshape(-1, 2)[pick].reshape(-1), exp).all()
+    assert (ss[pick] == ess).all()
+    g, _ = xb.extend_tasks(pool, ds.tasks, ds.k, ds.band, exec_flags=128)  # lane-group escalations
+    assert result_rows_equal(g, out).all()
