@@ -921,7 +921,6 @@ static int run_plan(xb_batch* B, DevBatch& D) {
     tp.band = B->band;
     tp.warp_scratch = D.d_scratch;
     tp.resume = D.d_resume;
-    tp.pat = 0x55555555u;
     tp.r64 = 64;
     tp.one = 1;
     tp.zero = 0;

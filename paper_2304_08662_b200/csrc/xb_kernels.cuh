@@ -65,7 +65,6 @@ struct TierParams {
     int32_t* __restrict__ resume;        // kResumeCap records of kResumeStride ints
     // opaque constants: kept in c[]/uniform registers so ptxas cannot fold
     // them into ALU-pipe forms (LEA, LOP3 immediates, SEL)
-    uint32_t pat;                        // 0x55555555
     int32_t r64;                         // 64
     int32_t one;                         // 1
     int32_t zero;                        // 0

@@ -3,12 +3,14 @@
 // semantics (proj/src/align.cpp:37-155); see xb_kernels.cuh for the
 // coordinate system, the drift-space values and the exact running-best chain.
 //
-// Per slot and antidiagonal the kernel issues 8 instructions split evenly
-// over the two integer pipes (B200 ALU pipe and FMA pipe, 16 lanes/clk per
-// SMSP each):
-//   ALU: LOP3 (match bits), VIMNMX3 (recurrence), VIADDMNMX (running best),
-//        ISETP (drop test)
-//   FMA: IMAD.HI (diag + sim), IMAD (slot key), @p IMAD (kill), @p IMAD (dead mask)
+// Per slot and antidiagonal the DNA kernel issues 7 instructions over the
+// two integer pipes (B200 ALU pipe and FMA pipe, 16 lanes/clk per SMSP each):
+//   ALU: VIMNMX3 (recurrence), VIADDMNMX (running best), ISETP (drop test)
+//   FMA: IDP.4A (diagonal + score), IMAD (slot key), @p IMAD (kill),
+//        @p IMAD (dead-mask bit)
+// plus ~10 per 16 slots building the match words, and ~70 per antidiagonal
+// of bookkeeping.  Table modes (other schemes) replace the IDP by a PRMT +
+// shared-table load.
 #include <climits>
 #include <cstdint>
 #include <utility>
