@@ -65,6 +65,7 @@ struct TierParams {
     int32_t* __restrict__ resume;        // kResumeCap records of kResumeStride ints
     // opaque constants: kept in c[]/uniform registers so ptxas cannot fold
     // them into ALU-pipe forms (LEA, LOP3 immediates, SEL)
+    uint32_t pad0;                       // keeps the constants below 8-byte paired (LDC.64)
     int32_t r64;                         // 64
     int32_t one;                         // 1
     int32_t zero;                        // 0
@@ -156,8 +157,12 @@ struct Reader {
     // before the next refill point
     __device__ __forceinline__ void init(const uint32_t* pool, int64_t pos, int d, int64_t t0, int r) {
         dir = d;
-        const uint32_t c = chunk_mem_e<ENC>(pool, d ? pos + t0 : pos - t0 - (F::PER - 1));
-        cur = (TOP ? (d != 0) : (d == 0)) ? rev_fields<ENC>(c) : c;
+        if constexpr (ENC == ENC_2BIT) {
+            cur = TOP ? chunk_tf(pool, pos, d, t0) : chunk_bf(pool, pos, d, t0);
+        } else {
+            const uint32_t c = chunk_mem_e<ENC>(pool, d ? pos + t0 : pos - t0 - (F::PER - 1));
+            cur = (TOP ? (d != 0) : (d == 0)) ? rev_fields<ENC>(c) : c;
+        }
         const int64_t q = d ? pos + t0 + r : pos - (t0 + r) - (F::PER - 1);
         const int64_t wi = q >> F::LOG;
         sh = uint32_t(q & (F::PER - 1)) * uint32_t(F::BITS);
