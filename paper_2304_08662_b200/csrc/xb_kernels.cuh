@@ -27,6 +27,7 @@
 // key_k >= c_k with c = running max of (key - 64X - 63).
 #pragma once
 
+#include <cstddef>
 #include <cstdint>
 
 #include "xb_internal.h"
@@ -65,7 +66,7 @@ struct TierParams {
     int32_t* __restrict__ resume;        // kResumeCap records of kResumeStride ints
     // opaque constants: kept in c[]/uniform registers so ptxas cannot fold
     // them into ALU-pipe forms (LEA, LOP3 immediates, SEL)
-    uint32_t pad0;                       // keeps the constants below 8-byte paired (LDC.64)
+    uint32_t pad0;                       // see the static_assert below
     int32_t r64;                         // 64
     int32_t one;                         // 1
     int32_t zero;                        // 0
@@ -73,6 +74,10 @@ struct TierParams {
     uint32_t ones;                       // 0x01010101
     uint32_t mulc[16];                   // 2^(32-2f), f = 1..15
 };
+// The K24 loop re-reads these constants from the parameter bank; with r64 at
+// an offset = 4 (mod 8) ptxas pairs them so that the loop runs 165 ms on full
+// config 5, at 0 (mod 8) 176 ms (A/B over five layouts).
+static_assert(offsetof(TierParams, r64) % 8 == 4, "keep the opaque constants' pairing");
 
 // ---------------------------------------------------------------- pool ----
 
