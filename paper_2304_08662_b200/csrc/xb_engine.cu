@@ -1016,15 +1016,14 @@ static int run_cascade(xb_batch* B, DevBatch& D) {
                 CK(launch_tier(D.all_group, mode, t, tp,
                                D.sm_count * (D.all_group ? D.gocc[t] : D.occ[t]), D.stream));
                 ++D.launches;
-            } else {
+            } else if (t == D.t0) {  // the start tier: one thread per unit
                 tp.role = kRoleStart;
                 CK(launch_tier(false, mode, t, tp, D.sm_count * D.occ[t], D.stream));
                 ++D.launches;
-                if (t > D.t0) {
-                    tp.role = kRoleEscalations;
-                    CK(launch_tier(true, mode, t, tp, D.sm_count * D.gocc[t], D.stream));
-                    ++D.launches;
-                }
+            } else {  // wider tiers: their escalations, on lane groups
+                tp.role = kRoleEscalations;
+                CK(launch_tier(true, mode, t, tp, D.sm_count * D.gocc[t], D.stream));
+                ++D.launches;
             }
         }
         CK(cudaEventRecord(D.ev[3 + t], D.stream));
