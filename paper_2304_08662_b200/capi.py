@@ -58,6 +58,18 @@ class XbExec(C.Structure):
 
 
 TIER_NAMES = ["thread_k16", "thread_k24", "thread_k32", "thread_k48", "thread_k64", "warp"]
+TIER_WIDTHS = [16, 24, 32, 48, 64]
+
+
+def tier_kernel_name(t: int, stats: dict, flags: int = 0) -> str:
+    """Kernel that served tier t in a run: the start tier runs one thread per
+    unit unless the batch was latency-bound (lane groups); wider tiers take
+    their escalations on lane groups (xb_engine.cu, run_cascade)."""
+    if t >= len(TIER_WIDTHS):
+        return "warp"
+    s = stats.get("start_tier", -1)
+    group = bool(flags & 32) or (t == s and stats.get("start_lane_groups")) or (t > s >= 0 and not flags & 64)
+    return f"{'group' if group else 'thread'}_k{TIER_WIDTHS[t]}"
 
 
 class XbStats(C.Structure):

@@ -997,6 +997,22 @@ __global__ void gather_patch_kernel(TierParams P, int t0, uint32_t* __restrict__
     }
 }
 
+// Resident lane-group blocks per SM for a latency-bound start tier.  A block
+// puts one warp (8 groups) on each SMSP.  A lone warp advances one step per
+// ~380 cycles of latency while issuing ~170 instructions, so a second warp per
+// SMSP fits in the latency shadow and a third only slows every step down --
+// including the longest unit's, which sets the batch's wall time.  Batches
+// that fit one block per SM keep one warp per SMSP: spreading the units over
+// more SMSPs shortens every step.  Measured on 1 B200 (scripts/lat_sweep.sh,
+// tier ms at 4/3/2/1 blocks): C1 0.57/0.45/0.35/0.31, C2 10.6/8.8/7.4/12.6,
+// C3 4.97/4.98/4.98/5.52.
+// XB_LATENCY_BLOCKS overrides the choice (the sweep).
+static int latency_blocks_per_sm(const DevBatch& D) {
+    if (const char* e = std::getenv("XB_LATENCY_BLOCKS")) return std::max(1, std::atoi(e));
+    const int64_t groups_per_block = kTB / kGroupLanes;
+    return D.n_units <= int64_t(D.sm_count) * groups_per_block ? 1 : 2;
+}
+
 // The cascade: the start tier takes the queue, wider tiers their
 // escalations, the warp tier whatever is left.  Once the start tier is done
 // every other row is final, so the results cross PCIe (copy stream) while
@@ -1013,8 +1029,9 @@ static int run_cascade(xb_batch* B, DevBatch& D) {
         if (t >= D.t0) {
             if (D.all_group || D.no_group) {
                 tp.role = kRoleAll;
-                CK(launch_tier(D.all_group, mode, t, tp,
-                               D.sm_count * (D.all_group ? D.gocc[t] : D.occ[t]), D.stream));
+                int per_sm = D.all_group ? D.gocc[t] : D.occ[t];
+                if (D.all_group && t == D.t0) per_sm = std::min(per_sm, latency_blocks_per_sm(D));
+                CK(launch_tier(D.all_group, mode, t, tp, D.sm_count * per_sm, D.stream));
                 ++D.launches;
             } else if (t == D.t0) {  // the start tier: one thread per unit
                 tp.role = kRoleStart;
