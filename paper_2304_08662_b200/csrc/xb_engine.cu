@@ -471,6 +471,21 @@ void xb_pool_free(xb_pool* p) {
 // Device buffers + pinned staging of one batch on one device.  Cached per
 // (pool, device) and reused by later batches, so repeated calls do not pay
 // cudaMalloc / page-locking on every step.
+// Throughput-planned batches fill every SM with persistent start-tier blocks,
+// so on one device their cascades run one after another: a batch's start
+// tier waits for the previous such batch's last kernel (its escalation tail
+// would otherwise starve behind the newer batch's resident blocks until that
+// whole start tier ends).  Their uploads and planning (prep, sort, pilot)
+// still overlap the previous batch.  Latency-planned batches are not ordered.
+struct CascadeOrder {
+    std::mutex mu;
+    std::map<int, cudaEvent_t> last;  // device -> event after the last ordered cascade
+};
+static CascadeOrder& cascade_order() {
+    static CascadeOrder* o = new CascadeOrder();
+    return *o;
+}
+
 struct Workspace {
     int dev = 0;
     bool in_use = false;
@@ -500,7 +515,7 @@ struct Workspace {
     DevResult* d_patch_res = nullptr;
     uint32_t* h_patch_idx = nullptr;
     DevResult* h_patch_res = nullptr;
-    int32_t* h_misc = nullptr;  // pinned: start tier read back after the pilot
+    int32_t* h_misc = nullptr;  // pinned (4 KiB): start tier after the pilot, counters, patch count
 
     void release_units() {
         cudaFree(d_units);
@@ -543,6 +558,12 @@ struct Workspace {
         capI = 0;
     }
     void destroy() {
+        {
+            CascadeOrder& o = cascade_order();
+            std::lock_guard<std::mutex> g(o.mu);
+            auto it = o.last.find(dev);
+            if (it != o.last.end() && it->second == ev[10]) o.last.erase(it);
+        }
         cudaSetDevice(dev);
         release_units();
         release_items();
@@ -685,7 +706,8 @@ static int setup_device(xb_batch* B, DevBatch& D, const xb_exec* ex) {
         CK(cudaMalloc(&W.d_ctr, sizeof(DevCounters)));
         CK(cudaMalloc(&W.d_resume, size_t(kResumeCap) * kResumeStride * 4));
         CK(cudaStreamCreateWithFlags(&W.copy_stream, cudaStreamNonBlocking));
-        CK(cudaMallocHost(&W.h_misc, 64));
+        CK(cudaMallocHost(&W.h_misc, 4096));
+        static_assert(sizeof(DevCounters) <= 4096, "h_misc holds the counters");
     }
     D.stream = (ex && ex->stream && B->devs.size() == 1) ? (cudaStream_t)ex->stream : W.stream;
     D.ev = W.ev;
@@ -1024,6 +1046,13 @@ static int run_cascade(xb_batch* B, DevBatch& D) {
     const int mode = D.mode;
     if (D.t0 < 0) D.t0 = D.h_misc[0];  // the stream was synchronised by xb_batch_run
     TierParams tp = D.tp;
+    std::unique_lock<std::mutex> order;
+    if (!D.all_group) {  // throughput-planned: after the previous such cascade
+        CascadeOrder& o = cascade_order();
+        order = std::unique_lock<std::mutex>(o.mu);
+        auto it = o.last.find(D.dev);
+        if (it != o.last.end()) CK(cudaStreamWaitEvent(D.stream, it->second, 0));
+    }
     for (int t = 0; t < 5; ++t) {
         tp.tier = t;
         if (t >= D.t0) {
@@ -1073,6 +1102,10 @@ static int run_cascade(xb_batch* B, DevBatch& D) {
                                                                        D.d_patch_res, D.capP);
         CK(cudaGetLastError());
         ++D.launches;
+    }
+    if (order.owns_lock()) {
+        CK(cudaEventRecord(D.ev[10], D.stream));
+        cascade_order().last[D.dev] = D.ev[10];
     }
     return XB_OK;
 }
@@ -1286,22 +1319,30 @@ int xb_batch_fetch(xb_batch* B, xb_side_result* out, int32_t* seed_score) {
                 for (int64_t q = 0; q < D.n_items; ++q) seed_score[D.tasks[size_t(q)]] = D.h_seed[q];
         }
         if (!D.early_copy) continue;
-        // rows finished after the start tier
-        CK(cudaStreamSynchronize(D.stream));
+        // rows finished after the start tier.  Every copy here is stream-
+        // ordered into pinned memory: a synchronous cudaMemcpy to pageable
+        // memory was seen to block until another batch's kernels on the
+        // device had finished (the batch stream, bench e2e).
         unsigned long long np = 0;
-        CK(cudaMemcpy(&np, &D.d_ctr->patch_n, 8, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpyAsync(D.h_misc, &D.d_ctr->patch_n, 8, cudaMemcpyDeviceToHost, D.stream));
+        CK(cudaStreamSynchronize(D.stream));
+        std::memcpy(&np, D.h_misc, 8);
         B->d2h += 8;
         if (int64_t(np) <= D.capP) {
             if (np) {
-                CK(cudaMemcpy(D.h_patch_idx, D.d_patch_idx, size_t(np) * 4, cudaMemcpyDeviceToHost));
-                CK(cudaMemcpy(D.h_patch_res, D.d_patch_res, size_t(np) * sizeof(DevResult),
-                              cudaMemcpyDeviceToHost));
+                CK(cudaMemcpyAsync(D.h_patch_idx, D.d_patch_idx, size_t(np) * 4, cudaMemcpyDeviceToHost,
+                                   D.stream));
+                CK(cudaMemcpyAsync(D.h_patch_res, D.d_patch_res, size_t(np) * sizeof(DevResult),
+                                   cudaMemcpyDeviceToHost, D.stream));
+                CK(cudaStreamSynchronize(D.stream));
                 B->d2h += int64_t(np) * int64_t(4 + sizeof(DevResult));
             }
             for (unsigned long long i = 0; i < np; ++i)
                 std::memcpy(&out[row(D.h_patch_idx[i])], &D.h_patch_res[i], sizeof(xb_side_result));
         } else {  // more late rows than patch slots: copy everything again
-            CK(cudaMemcpy(D.h_res, D.d_res, size_t(D.n_units) * sizeof(DevResult), cudaMemcpyDeviceToHost));
+            CK(cudaMemcpyAsync(D.h_res, D.d_res, size_t(D.n_units) * sizeof(DevResult), cudaMemcpyDeviceToHost,
+                               D.stream));
+            CK(cudaStreamSynchronize(D.stream));
             B->d2h += D.n_units * int64_t(sizeof(DevResult));
             copy_rows(D.h_res);
         }
@@ -1318,7 +1359,9 @@ int xb_batch_stats(xb_batch* B, xb_stats* st) {
         CK(cudaSetDevice(D.dev));
         CK(cudaStreamSynchronize(D.stream));
         DevCounters c{};
-        CK(cudaMemcpy(&c, D.d_ctr, sizeof c, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpyAsync(D.h_misc, D.d_ctr, sizeof c, cudaMemcpyDeviceToHost, D.stream));
+        CK(cudaStreamSynchronize(D.stream));
+        std::memcpy(&c, D.h_misc, sizeof c);
         float ms[10] = {0};
         if (D.n_units) {
             CK(cudaEventElapsedTime(&ms[0], D.ev[0], D.ev[8]));  // whole run

@@ -454,6 +454,62 @@ def extend_tasks(pool: DevicePool, tasks, k: int, band: int, exec_flags: int = 0
     return out, ss
 
 
+def extend_batches(batches, k: int, band: int, exec_flags: int = 0, n_devices: int = 1,
+                   device_ids=None, reupload: bool = False, stats: list | None = None):
+    """A stream of batches through the device-resident batch C-ABI
+    (xb_batch_create / run / fetch), one batch in flight ahead of the host:
+    batch i+1's uploads (pool if not resident, tasks) and planning overlap
+    batch i's kernels, and batch i's rows are copied out while batch i+1
+    runs.  `batches` yields (DevicePool, tasks); yields (results[2n],
+    seed_score[n]) per batch, in order.  reupload=True drops each batch's
+    device pool copy before its upload (xb_pool_evict), so every batch's
+    inputs cross PCIe -- consecutive batches must then use distinct pools,
+    since batch i may still read its pool while batch i+1 uploads.  `stats`,
+    if given, receives each batch's xb_stats dict."""
+    L = lib()
+    ex = capi.make_exec(n_devices, device_ids, None, exec_flags)
+    prev = None  # (handle, pool, results, seeds)
+
+    def finish(p):
+        h, _, out, ss = p
+        try:
+            _raise(L.xb_batch_fetch(h, out.ctypes.data, ss.ctypes.data), "xb_batch_fetch")
+            if stats is not None:
+                st = capi.XbStats()
+                _raise(L.xb_batch_stats(h, C.byref(st)), "xb_batch_stats")
+                stats.append(st.as_dict())
+        finally:
+            L.xb_batch_free(h)
+        return out, ss
+
+    try:
+        for pool, tasks in batches:
+            if reupload:
+                if prev is not None and prev[1] is pool:
+                    raise ValueError("reupload: consecutive batches need distinct pools")
+                pool.evict()
+            t = tasks_array(tasks)
+            err, bad = C.c_int(0), C.c_int64(-1)
+            h = L.xb_batch_create(pool._h, t.ctypes.data, len(t), k, band, C.byref(ex),
+                                  C.byref(bad), C.byref(err))
+            _raise(err.value, "xb_batch_create", bad.value)
+            cur = (h, pool, np.zeros(2 * len(t), dtype=RESULT_DTYPE), np.zeros(len(t), dtype=np.int32))
+            rc = L.xb_batch_run(h)
+            if rc:
+                L.xb_batch_free(h)
+                _raise(rc, "xb_batch_run")
+            if prev is not None:
+                p, prev = prev, None
+                yield finish(p)
+            prev = cur
+        if prev is not None:
+            p, prev = prev, None
+            yield finish(p)
+    finally:
+        if prev is not None:
+            L.xb_batch_free(prev[0])
+
+
 # ---------------------------------------------------------------- ingest ----
 # proj/src/io.cpp:58-196, native (csrc/xb_ingest.cpp)
 

@@ -38,3 +38,30 @@ for rep in range(3):
     print(f"create {1e3*(t1-t0):.1f} ms  run-launch {1e3*(t2-t1):.1f}  sync {1e3*(t3-t2):.1f}  "
           f"fetch {1e3*(t4-t3):.1f}  free {1e3*(t5-t4):.1f}  total {1e3*(t5-t0):.1f}  device {st.ms_total:.1f}  "
           f"h2d {st.h2d_bytes/1e6:.0f} MB", flush=True)
+
+# the batch stream (bench e2e): host phases of each batch, one batch in flight ahead
+pools = [pool, xb.DevicePool(s, ds.symbols, ds.offsets)]
+for n_batches in (2, 6):
+    t0 = time.perf_counter()
+    ms = lambda: 1e3 * (time.perf_counter() - t0)  # noqa: E731
+    prev, log = None, []
+    for i in range(n_batches + 1):
+        if i < n_batches:
+            pools[i % 2].evict()
+            err, bad = C.c_int(0), C.c_int64(-1)
+            a = ms()
+            h = L.xb_batch_create(pools[i % 2]._h, t.ctypes.data, len(t), ds.k, ds.band, C.byref(ex),
+                                  C.byref(bad), C.byref(err))
+            b = ms()
+            capi.check(L.xb_batch_run(h), "run")
+            c = ms()
+            log.append(f"b{i}: create {a:.0f}-{b:.0f} run -{c:.0f}")
+        if prev is not None:
+            a = ms()
+            capi.check(L.xb_batch_fetch(prev, out.ctypes.data, ss.ctypes.data), "fetch")
+            st = capi.XbStats()
+            L.xb_batch_stats(prev, C.byref(st))
+            L.xb_batch_free(prev)
+            log.append(f"fetch b{i-1} {a:.0f}-{ms():.0f} (device {st.ms_total:.1f})")
+        prev = h if i < n_batches else None
+    print(f"stream of {n_batches}: wall {ms():.0f} ms: " + "; ".join(log), flush=True)

@@ -293,6 +293,30 @@ def test_multi_device_sharding_same_results(xb):
     assert st["n_devices"] == 2
 
 
+def test_batch_stream_same_results(xb):
+    """extend_batches (one batch in flight ahead, pools re-uploaded every
+    batch) returns, for each batch, exactly the synchronous call's rows;
+    throughput-planned and latency-planned batches mixed in one stream."""
+    from paper_2304_08662_b200 import synth
+    ds = synth.make(5, 0.01)
+    pools = [_config_pool(xb, ds), _config_pool(xb, ds)]
+    cuts = [ds.tasks, ds.tasks[:500], ds.tasks[7:20000], ds.tasks]
+    want = [xb.extend_tasks(pools[0], t, ds.k, ds.band) for t in cuts]
+    stats = []
+    got = list(xb.xband.extend_batches(((pools[i % 2], t) for i, t in enumerate(cuts)), ds.k, ds.band,
+                                       reupload=True, stats=stats))
+    assert len(got) == len(cuts) == len(stats)
+    for (a, sa), (b, sb) in zip(want, got):
+        assert result_rows_equal(a, b).all() and (sa == sb).all()
+    assert all(s["h2d_bytes"] > 0 for s in stats)  # every batch re-uploaded its pool
+    with pytest.raises(ValueError):  # one pool cannot be re-uploaded under an in-flight batch
+        list(xb.xband.extend_batches(((pools[0], t) for t in cuts[:2]), ds.k, ds.band, reupload=True))
+    # without re-upload one pool serves the whole stream
+    got = list(xb.xband.extend_batches(((pools[0], t) for t in cuts), ds.k, ds.band))
+    for (a, sa), (b, sb) in zip(want, got):
+        assert result_rows_equal(a, b).all() and (sa == sb).all()
+
+
 def test_sweep_band_matches_reference(xb):
     """§8(f) band survey on the GPU (pipeline.cpp:181-208): the reference's TSV
     byte for byte, including acceptance criterion 2 (L=20000, p=0.9, X=15:
