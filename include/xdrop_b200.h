@@ -84,6 +84,7 @@ typedef struct {
 #define XB_FLAG_GROUP 32        /* every thread-tier launch runs as lane groups (testing) */
 #define XB_FLAG_NO_GROUP 64     /* never use lane groups: one thread per unit throughout (ablation) */
 #define XB_FLAG_THROUGHPUT 128  /* plan a small batch like a large one: pilot + cost model (testing) */
+#define XB_FLAG_SERIAL_TAIL 4096 /* wider tiers only after the start tier (no concurrent escalation consumer; ablation) */
 
 /* Per-call device statistics (summed over devices; times are the max).
  * Tiers: 0..4 = one unit per thread with a K = 16/24/32/48/64 slot band,

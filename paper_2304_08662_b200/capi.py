@@ -35,6 +35,7 @@ XB_FLAG_ESC_TO_WARP = 16
 XB_FLAG_GROUP = 32
 XB_FLAG_NO_GROUP = 64
 XB_FLAG_THROUGHPUT = 128
+XB_FLAG_SERIAL_TAIL = 4096
 
 
 def force_tier(t: int) -> int:

@@ -32,7 +32,7 @@ template <int K, int G, int MODE>
 __global__ void group_tier_kernel(TierParams P);
 template <int ENC>
 __global__ void warp_tier_kernel(TierParams P);
-__global__ void select_tier_kernel(TierParams P, int forced);
+__global__ void select_tier_kernel(TierParams P, int forced, int32_t* host_out);
 __global__ void prep_kernel(PrepParams P);
 __global__ void int_peak_alu(int32_t* out, int iters, int32_t seed, long long* clk);
 __global__ void int_peak_mixed(int32_t* out, int iters, int32_t seed, long long* clk);
@@ -486,6 +486,10 @@ static CascadeOrder& cascade_order() {
     return *o;
 }
 
+// h_misc (pinned, 4 KiB per workspace): counters and the patch count are
+// copied to its start; the pilot's start tier is written by the kernel here.
+constexpr int kMiscStartTier = 1000;
+
 struct Workspace {
     int dev = 0;
     bool in_use = false;
@@ -510,6 +514,8 @@ struct Workspace {
     // rows finished after the start tier (escalations, warp tier), gathered
     // so that the bulk of the results can cross PCIe during the cascade tail
     cudaStream_t copy_stream = nullptr;
+    cudaStream_t aux_stream = nullptr;  // high priority: the concurrent escalation consumer
+    cudaEvent_t aux_ev[2] = {};
     int64_t capP = 0;
     uint32_t* d_patch_idx = nullptr;
     DevResult* d_patch_res = nullptr;
@@ -575,6 +581,9 @@ struct Workspace {
             if (e) cudaEventDestroy(e);
         if (stream) cudaStreamDestroy(stream);
         if (copy_stream) cudaStreamDestroy(copy_stream);
+        if (aux_stream) cudaStreamDestroy(aux_stream);
+        for (auto& e : aux_ev)
+            if (e) cudaEventDestroy(e);
     }
 };
 
@@ -583,6 +592,8 @@ struct DevBatch {
     int dev = 0;
     cudaStream_t stream = nullptr;
     cudaStream_t copy_stream = nullptr;
+    cudaStream_t aux_stream = nullptr;
+    cudaEvent_t* aux_ev = nullptr;
     int t0 = -1;               // start tier, when known on the host
     bool early_copy = false;   // results copied after the start tier, patched at fetch
     int64_t capP = 0;
@@ -706,6 +717,10 @@ static int setup_device(xb_batch* B, DevBatch& D, const xb_exec* ex) {
         CK(cudaMalloc(&W.d_ctr, sizeof(DevCounters)));
         CK(cudaMalloc(&W.d_resume, size_t(kResumeCap) * kResumeStride * 4));
         CK(cudaStreamCreateWithFlags(&W.copy_stream, cudaStreamNonBlocking));
+        int lo_pri = 0, hi_pri = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri));
+        CK(cudaStreamCreateWithPriority(&W.aux_stream, cudaStreamNonBlocking, hi_pri));
+        for (auto& e : W.aux_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         CK(cudaMallocHost(&W.h_misc, 4096));
         static_assert(sizeof(DevCounters) <= 4096, "h_misc holds the counters");
     }
@@ -775,6 +790,8 @@ static int setup_device(xb_batch* B, DevBatch& D, const xb_exec* ex) {
     D.d_scratch = W.d_scratch;
     D.d_resume = W.d_resume;
     D.copy_stream = W.copy_stream;
+    D.aux_stream = W.aux_stream;
+    D.aux_ev = W.aux_ev;
     D.capP = W.capP;
     D.d_patch_idx = W.d_patch_idx;
     D.d_patch_res = W.d_patch_res;
@@ -986,7 +1003,8 @@ static int run_plan(xb_batch* B, DevBatch& D) {
         ++D.launches;
     }
     tp.pilot = 0;
-    select_tier_kernel<<<1, 32, 0, D.stream>>>(tp, forced >= 0 ? forced : (pn > 0 ? -1 : default_start));
+    select_tier_kernel<<<1, 256, 0, D.stream>>>(tp, forced >= 0 ? forced : (pn > 0 ? -1 : default_start),
+                                                D.h_misc + kMiscStartTier);
     CK(cudaGetLastError());
     ++D.launches;
     CK(cudaEventRecord(D.ev[2], D.stream));
@@ -994,9 +1012,7 @@ static int run_plan(xb_batch* B, DevBatch& D) {
     D.all_group = all_group;
     D.no_group = no_group;
     D.t0 = forced >= 0 ? forced : (pn > 0 ? -1 : default_start);  // -1: read back after the pilot
-    if (D.t0 < 0)
-        CK(cudaMemcpyAsync(D.h_misc, &D.d_ctr->start_tier, 4, cudaMemcpyDeviceToHost, D.stream));
-    return XB_OK;
+    return XB_OK;  // a pilot-chosen start tier arrives in h_misc[kMiscStartTier] (written by the kernel)
 }
 
 __global__ void gather_patch_kernel(TierParams P, int t0, uint32_t* __restrict__ idx,
@@ -1028,6 +1044,12 @@ __global__ void gather_patch_kernel(TierParams P, int t0, uint32_t* __restrict__
 // more SMSPs shortens every step.  Measured on 1 B200 (scripts/lat_sweep.sh,
 // tier ms at 4/3/2/1 blocks): C1 0.57/0.45/0.35/0.31, C2 10.6/8.8/7.4/12.6,
 // C3 4.97/4.98/4.98/5.52.
+// Lane-group blocks that consume the next tier's escalations while a
+// throughput start tier runs.  Each one displaces about one start-tier block
+// (1/592 of the machine); 4 blocks serve 128 escalated units at a time, which
+// keeps up with config 5's ~3,000 escalations over the 165 ms start tier.
+constexpr int kConsumerBlocks = 4;
+
 // XB_LATENCY_BLOCKS overrides the choice (the sweep).
 static int latency_blocks_per_sm(const DevBatch& D) {
     if (const char* e = std::getenv("XB_LATENCY_BLOCKS")) return std::max(1, std::atoi(e));
@@ -1044,8 +1066,13 @@ static int run_cascade(xb_batch* B, DevBatch& D) {
     CK(cudaSetDevice(D.dev));
     xb_pool* p = B->pool;
     const int mode = D.mode;
-    if (D.t0 < 0) D.t0 = D.h_misc[0];  // the stream was synchronised by xb_batch_run
+    if (D.t0 < 0) D.t0 = D.h_misc[kMiscStartTier];  // the stream was synchronised by xb_batch_run
     TierParams tp = D.tp;
+    // the next tier's escalations are consumed concurrently with the start
+    // tier (lane groups, when there is a wider lane-group tier); the
+    // kRoleEscalations launch after the start tier finishes what is left
+    const bool concurrent = !D.all_group && !D.no_group && D.t0 + 1 < 5 &&
+                            !(B->flags & (XB_FLAG_ESC_TO_WARP | XB_FLAG_SERIAL_TAIL));
     std::unique_lock<std::mutex> order;
     if (!D.all_group) {  // throughput-planned: after the previous such cascade
         CascadeOrder& o = cascade_order();
@@ -1063,13 +1090,32 @@ static int run_cascade(xb_batch* B, DevBatch& D) {
                 CK(launch_tier(D.all_group, mode, t, tp, D.sm_count * per_sm, D.stream));
                 ++D.launches;
             } else if (t == D.t0) {  // the start tier: one thread per unit
+                if (concurrent) {
+                    // the next tier's list starts empty-marked; a few high-priority
+                    // lane-group blocks take its escalations while this tier runs
+                    CK(cudaMemsetAsync(D.d_lists + int64_t(t + 1) * D.n_units, 0xFF, size_t(D.n_units) * 4,
+                                       D.stream));
+                    CK(cudaEventRecord(D.aux_ev[0], D.stream));
+                    CK(cudaStreamWaitEvent(D.aux_stream, D.aux_ev[0], 0));
+                    TierParams cp = tp;
+                    cp.tier = t + 1;
+                    cp.role = kRoleConsumer;
+                    CK(launch_tier(true, mode, t + 1, cp, kConsumerBlocks, D.aux_stream));
+                    CK(cudaEventRecord(D.aux_ev[1], D.aux_stream));
+                    ++D.launches;
+                }
                 tp.role = kRoleStart;
-                CK(launch_tier(false, mode, t, tp, D.sm_count * D.occ[t], D.stream));
+                // leave the consumer's blocks room to be resident whichever kernel
+                // the hardware dispatches first (start-tier blocks are persistent)
+                CK(launch_tier(false, mode, t, tp,
+                               std::max(1, D.sm_count * D.occ[t] - (concurrent ? kConsumerBlocks : 0)),
+                               D.stream));
                 ++D.launches;
             } else {  // wider tiers: their escalations, on lane groups
                 tp.role = kRoleEscalations;
                 CK(launch_tier(true, mode, t, tp, D.sm_count * D.gocc[t], D.stream));
                 ++D.launches;
+                if (concurrent && t == D.t0 + 1) CK(cudaStreamWaitEvent(D.stream, D.aux_ev[1], 0));
             }
         }
         CK(cudaEventRecord(D.ev[3 + t], D.stream));

@@ -531,24 +531,64 @@ __global__ void __launch_bounds__(128) group_tier_kernel(TierParams P) {
 #pragma unroll
     for (int s = 0; s < SS; ++s) E[s] = O[s] = kDeadS;
     bool active = false;
+    // kRoleConsumer: the list grows while this kernel runs.  A group claims
+    // a slot only once the list is longer than the cursor (so it never holds
+    // a claim it cannot serve and may stop at any time: the kRoleEscalations
+    // launch after the start tier takes whatever is left), waits for the
+    // claimed slot's entry to be written, and idles while nothing is queued.
+    const bool consumer = P.role == kRoleConsumer;
+    bool waiting = consumer;  // a consumer group with no unit, still looking for one
     unsigned it = 0xFFFFFFFFu;
     auto fetch = [&]() {
         active = false;
         for (;;) {
             unsigned long long i = 0;
-            if (lane == 0) i = atomicAdd(Q.cursor, 1ull);
-            i = __shfl_sync(gmask, i, 0, G);
-            if (i >= Q.len) {
-                S.stop = kDone;
-                S.m = S.n = 0;
-                return;
+            uint32_t e = 0;
+            if (consumer) {
+                int st = 0;  // 0 nothing queued, 1 claimed slot i (entry e), 2 start tier done
+                if (lane == 0) {
+                    volatile unsigned long long* lenp = &P.ctr->list_len[P.tier];
+                    volatile unsigned long long* curp = Q.cursor;
+                    for (;;) {
+                        const unsigned long long c = *curp;
+                        if (c >= *lenp) {
+                            st = *(volatile int32_t*)&P.ctr->prod_finished ? 2 : 0;
+                            break;
+                        }
+                        if (atomicCAS(Q.cursor, c, c + 1) == c) {
+                            i = c;
+                            const volatile uint32_t* ep = Q.q + (long long)i;
+                            while ((e = *ep) == kEmptyEntry) __nanosleep(64);
+                            __threadfence();  // the entry's resume record is visible past this point
+                            st = 1;
+                            break;
+                        }
+                    }
+                }
+                st = __shfl_sync(gmask, st, 0, G);
+                if (st != 1) {
+                    waiting = st == 0;
+                    S.stop = kDone;
+                    S.m = S.n = 0;
+                    return;
+                }
+                i = __shfl_sync(gmask, i, 0, G);
+                e = __shfl_sync(gmask, e, 0, G);
+            } else {
+                if (lane == 0) i = atomicAdd(Q.cursor, 1ull);
+                i = __shfl_sync(gmask, i, 0, G);
+                if (i >= Q.len) {
+                    S.stop = kDone;
+                    S.m = S.n = 0;
+                    return;
+                }
+                e = Q.q[(long long)i * Q.stride];
             }
-            const uint32_t e = Q.q[(long long)i * Q.stride];
             uint32_t unit = e;
             const int32_t* rec = nullptr;
             if (e & kResumeFlag) {
                 rec = P.resume + (long long)(e & ~kResumeFlag) * kResumeStride;
-                unit = uint32_t(rec[kRecUnit]);
+                unit = uint32_t(__ldcg(rec + kRecUnit));
             }
             const DevUnit u = P.units[unit];
             if (u.route != 0) {
@@ -585,16 +625,16 @@ __global__ void __launch_bounds__(128) group_tier_kernel(TierParams P) {
                 g_windows(S, P.pool, lane, r, r);
             } else {
                 // continue from a narrower tier's record (see resume_unit)
-                const int ko = rec[kRecK];
+                const int ko = __ldcg(rec + kRecK);
                 const int off = (K - ko) >> 1;
-                const int d = rec[kRecD];
-                S.ubase = rec[kRecUbase] - off;
-                S.Tc = rec[kRecTc];
-                S.best_d = rec[kRecBestD];
-                S.best_u = rec[kRecBestU];
-                S.cells = rec[kRecCells];
-                S.delta_w = rec[kRecDeltaW];
-                const int h1 = rec[kRecHs1], l1 = rec[kRecLs1], h2 = rec[kRecHs2], l2 = rec[kRecLs2];
+                const int d = __ldcg(rec + kRecD);
+                S.ubase = __ldcg(rec + kRecUbase) - off;
+                S.Tc = __ldcg(rec + kRecTc);
+                S.best_d = __ldcg(rec + kRecBestD);
+                S.best_u = __ldcg(rec + kRecBestU);
+                S.cells = __ldcg(rec + kRecCells);
+                S.delta_w = __ldcg(rec + kRecDeltaW);
+                const int h1 = __ldcg(rec + kRecHs1), l1 = __ldcg(rec + kRecLs1), h2 = __ldcg(rec + kRecHs2), l2 = __ldcg(rec + kRecLs2);
                 S.hs1 = h1 < 0 ? -1 : h1 + off;
                 S.lr1 = h1 < 0 ? -1 : KB - (l1 + off);
                 S.hs2 = h2 < 0 ? -1 : h2 + off;
@@ -604,8 +644,8 @@ __global__ void __launch_bounds__(128) group_tier_kernel(TierParams P) {
                 for (int s = 0; s < SS; ++s) {
                     const int src = k0 + s - off;
                     const bool in = src >= 0 && src < ko;
-                    const int32_t vc = in ? rec[kRecRows + src] : kDeadS;
-                    const int32_t vp = in ? rec[kRecRows + ko + src] : kDeadS;
+                    const int32_t vc = in ? __ldcg(rec + kRecRows + src) : kDeadS;
+                    const int32_t vp = in ? __ldcg(rec + kRecRows + ko + src) : kDeadS;
                     O[s] = odd ? vc : vp;
                     E[s] = odd ? vp : vc;
                 }
@@ -620,7 +660,13 @@ __global__ void __launch_bounds__(128) group_tier_kernel(TierParams P) {
     };
     fetch();
     it = 0;
-    while (__any_sync(0xFFFFFFFFu, active)) {
+    while (__any_sync(0xFFFFFFFFu, active || waiting)) {
+        if (consumer && !__any_sync(0xFFFFFFFFu, active)) {  // nothing queued for this warp yet
+            __nanosleep(2000);
+            if (waiting) fetch();
+            ++it;
+            continue;
+        }
         if (active && (it & (St::RPER - 1)) == 0) {
             if (lane == 0) S.rv.refill(P.pool);
             if (lane == G - 1) S.rh.refill(P.pool);
@@ -635,7 +681,8 @@ __global__ void __launch_bounds__(128) group_tier_kernel(TierParams P) {
             gstep<K, G, MODE, true, true>(S, O, E, P, tab, gap, X, it, lane, gmask, sk);
         }
         gstep<K, G, MODE, false, true>(S, E, O, P, tab, gap, X, it, lane, gmask, sk);
-        if (active && S.stop) fetch();  // outcome already recorded by the deciding step
+        // outcome recorded by the deciding step; idle consumer groups poll every 8th iteration
+        if ((active && S.stop) || (!active && waiting && (it & 7) == 0)) fetch();
         ++it;
     }
     if (P.pilot || lane != 0) return;

@@ -60,6 +60,8 @@ struct DevCounters {
     int32_t pad;
     unsigned long long resume_next;    // resume records handed out
     unsigned long long patch_n;        // result rows finalised after the start tier
+    unsigned int prod_done;            // start-tier blocks finished (concurrent escalation tail)
+    int32_t prod_finished;             // 1 once every start-tier block has finished
 };
 
 // Resume records: a unit that outgrows its tier saves its band state at the

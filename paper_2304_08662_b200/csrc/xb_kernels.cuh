@@ -252,7 +252,11 @@ struct PrepParams {
 
 // Queue roles of a tier launch: a tier can be served by the thread kernel
 // for its main queue and by the lane-group kernel for its escalations.
-enum : int { kRoleAll = 0, kRoleStart = 1, kRoleEscalations = 2 };
+// kRoleConsumer: a few lane-group blocks that take the next tier's
+// escalations WHILE the start tier still runs (the start tier publishes them
+// with kEmptyEntry-initialised slots), leaving kRoleEscalations a short tail.
+enum : int { kRoleAll = 0, kRoleStart = 1, kRoleEscalations = 2, kRoleConsumer = 3 };
+constexpr uint32_t kEmptyEntry = 0xFFFFFFFFu;  // escalation-list slot not yet written
 
 // Work source of a launch.  Pilot: a strided sample of the order.  Cascade:
 // the start tier takes the whole main queue, each wider tier the units
@@ -282,9 +286,12 @@ __device__ __forceinline__ bool make_queue(const TierParams& P, Queue& Q) {
     const int t0 = P.ctr->start_tier;
     if (P.tier < t0) return false;
     if (P.role == kRoleStart && P.tier != t0) return false;
-    if (P.role == kRoleEscalations && P.tier == t0) return false;
+    if ((P.role == kRoleEscalations || P.role == kRoleConsumer) && P.tier == t0) return false;
     Q.cursor = &P.ctr->cursor[P.tier];
-    if (P.tier == t0) {
+    if (P.role == kRoleConsumer) {  // length read as it grows (consumer_claim)
+        Q.q = P.lists + (long long)P.tier * P.n_units;
+        Q.len = 0;
+    } else if (P.tier == t0) {
         Q.q = P.order;
         Q.len = (unsigned long long)P.n_units;
     } else {

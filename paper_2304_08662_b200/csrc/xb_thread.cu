@@ -373,8 +373,11 @@ __device__ __forceinline__ void finish_unit(TState<K, MODE>& S, const TierParams
     }
     if (code == kEscalate) {
         const uint32_t entry = sk.resumable ? save_resume(S, cur, prv, P, beta) : uint32_t(S.unit);
+        // a concurrent consumer may take the entry as soon as it is written:
+        // the record first, then the slot, then the entry (volatile)
+        __threadfence();
         const unsigned long long slot = atomicAdd(sk.esc_len, 1ull);
-        sk.esc_list[slot] = entry;
+        *(volatile uint32_t*)&sk.esc_list[slot] = entry;
         ++sk.esc;
         return;
     }
@@ -685,6 +688,13 @@ __global__ void __launch_bounds__(kTB, tier_min_blocks<K, MODE>()) thread_tier_k
     if (sk.units) atomicAdd(&P.ctr->units[P.tier], sk.units);
     if (sk.cells) atomicAdd(&P.ctr->cells[P.tier], sk.cells);
     if (sk.esc) atomicAdd(&P.ctr->escalated[P.tier], sk.esc);
+    if (P.role == kRoleStart) {  // tell a concurrent escalation consumer when the last block is done
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            if (atomicAdd(&P.ctr->prod_done, 1u) == gridDim.x - 1) atomicExch(&P.ctr->prod_finished, 1);
+        }
+    }
 }
 
 #define XB_INST(K)                                                   \
@@ -700,32 +710,49 @@ XB_INST(64)
 
 // Picks the start tier from the pilot sample: the width that minimises
 // K_t + sum over wider tiers of (share escalating into them) * 1.5 * K.
-__global__ void select_tier_kernel(TierParams P, int forced) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// One block: the sample is counted by all threads, thread 0 decides.  The
+// choice also goes straight to pinned host memory (host_out), so the host's
+// read-back does not queue behind other batches' copies on a copy engine.
+__global__ void select_tier_kernel(TierParams P, int forced, int32_t* host_out) {
+    __shared__ unsigned long long need[6];  // sample units needing more than tier t
+    __shared__ unsigned long long nn;
+    if (blockIdx.x != 0) return;
     if (forced >= 0) {
-        P.ctr->start_tier = forced;
+        if (threadIdx.x == 0) {
+            P.ctr->start_tier = forced;
+            *(volatile int32_t*)host_out = forced;
+        }
         return;
     }
-    long long need[6] = {0, 0, 0, 0, 0, 0};  // sample units needing more than tier t
-    long long n = 0;
-    for (long long q = 0; q < P.pilot_n; ++q) {
+    if (threadIdx.x < 6) need[threadIdx.x] = 0;
+    if (threadIdx.x == 0) nn = 0;
+    __syncthreads();
+    unsigned long long my_need[5] = {0, 0, 0, 0, 0}, my_n = 0;
+    for (long long q = threadIdx.x; q < P.pilot_n; q += blockDim.x) {
         const int pw = P.pilot_w[q];
         if (pw == -2) continue;
         const int w = pw < 0 ? (1 << 30) : pw + 2;  // +2: unclamped-window slack
-        ++n;
-        for (int t = 0; t < 5; ++t) need[t] += w > tier_width(t) && P.band > tier_width(t);
+        ++my_n;
+        for (int t = 0; t < 5; ++t) my_need[t] += w > tier_width(t) && P.band > tier_width(t);
     }
+    for (int t = 0; t < 5; ++t)
+        if (my_need[t]) atomicAdd(&need[t], my_need[t]);
+    if (my_n) atomicAdd(&nn, my_n);
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    const double n = double(nn);
     int best = 4;
     double best_cost = 1e30;
     for (int t = 0; t < 5; ++t) {
         double cost = tier_width(t);
-        for (int u = t + 1; u < 5; ++u) cost += 1.5 * tier_width(u) * (n ? double(need[u - 1]) / n : 0.0);
+        for (int u = t + 1; u < 5; ++u) cost += 1.5 * tier_width(u) * (n > 0 ? double(need[u - 1]) / n : 0.0);
         if (cost < best_cost) {
             best_cost = cost;
             best = t;
         }
     }
     P.ctr->start_tier = best;
+    *(volatile int32_t*)host_out = best;
 }
 
 }  // namespace xb

@@ -176,8 +176,10 @@ def test_configs_sample_vs_oracle_full_size(xb, oracle, cfg):
     assert (ss == ess).all()
     a, _ = xb.extend_tasks(pool, ds.tasks, ds.k, ds.band)
     # unsorted, lane groups throughout, one thread per unit, and K16 starts whose
-    # escalations resume from saved records (past the record capacity on config 5)
-    for flags in (1, 32, 64, 64 | 8, 32 | 8):
+    # escalations resume from saved records (past the record capacity on config 5);
+    # K16 starts whose escalations a concurrent consumer takes while the start
+    # tier runs (8: most units escalate) and the serial tail (4096)
+    for flags in (1, 32, 64, 64 | 8, 32 | 8, 8, 4096, 8 | 4096):
         b, _ = xb.extend_tasks(pool, ds.tasks, ds.k, ds.band, exec_flags=flags)
         assert result_rows_equal(a, b).all(), flags
     # every sampled row inside the full run equals the sampled run
