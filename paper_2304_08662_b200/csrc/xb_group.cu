@@ -40,6 +40,12 @@ __device__ __forceinline__ int gbfind64(uint64_t x) {
     asm("bfind.u64 %0, %1;" : "=r"(r) : "l"(x));
     return r;
 }
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 template <int LUT>
 __device__ __forceinline__ uint32_t glop3(uint32_t a, uint32_t b, uint32_t c) {
     uint32_t d;
@@ -538,6 +544,10 @@ __global__ void __launch_bounds__(128) group_tier_kernel(TierParams P) {
     // claimed slot's entry to be written, and idles while nothing is queued.
     const bool consumer = P.role == kRoleConsumer;
     bool waiting = consumer;  // a consumer group with no unit, still looking for one
+    // Under serialising tools (ncu, compute-sanitizer) the start tier cannot
+    // run next to the consumer: if it has not started 5 ms after the consumer
+    // did, the consumer leaves everything to the kRoleEscalations launch.
+    const unsigned long long t_start = consumer ? globaltimer_ns() : 0ull;
     unsigned it = 0xFFFFFFFFu;
     auto fetch = [&]() {
         active = false;
@@ -552,7 +562,10 @@ __global__ void __launch_bounds__(128) group_tier_kernel(TierParams P) {
                     for (;;) {
                         const unsigned long long c = *curp;
                         if (c >= *lenp) {
-                            st = *(volatile int32_t*)&P.ctr->prod_finished ? 2 : 0;
+                            // the start tier (tier - 1) has taken no unit from its queue yet
+                            const bool alone = !*(volatile unsigned long long*)&P.ctr->cursor[P.tier - 1] &&
+                                               globaltimer_ns() - t_start > 5000000ull;
+                            st = (*(volatile int32_t*)&P.ctr->prod_finished || alone) ? 2 : 0;
                             break;
                         }
                         if (atomicCAS(Q.cursor, c, c + 1) == c) {
