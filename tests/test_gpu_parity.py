@@ -413,3 +413,29 @@ def test_table_modes_at_throughput_scale(xb, oracle, case):
     assert (ss[pick] == ess).all()
     g, _ = xb.extend_tasks(pool, ds.tasks, ds.k, ds.band, exec_flags=128)  # lane-group escalations
     assert result_rows_equal(g, out).all()
+
+
+def test_config5_full_size(xb, oracle):
+    """Config 5 at BASELINE size (2,000,000 extensions, 2.43e11 cells), the
+    bench workload: a seeded sample of 3000 tasks against the oracle; the
+    concurrent escalation consumer and the serial tail give identical rows;
+    size-independent properties of the whole batch (every side OK, cells
+    and delta_w within the band, stats consistent with the rows)."""
+    from paper_2304_08662_b200 import synth
+    ds = synth.make(5, 1.0)
+    assert ds.n_tasks == 2_000_000
+    pool = _config_pool(xb, ds)
+    out, ss = xb.extend_tasks(pool, ds.tasks, ds.k, ds.band)
+    st = xb.xband.last_stats()
+    assert not st["start_lane_groups"] and sum(st["units_tier"]) == 2 * ds.n_tasks
+    assert sum(st["cells_tier"]) == int(out["cells"].sum())
+    assert (out["status"] == 0).all() and (out["delta_w"] <= ds.band).all()
+    rng = np.random.default_rng(5)
+    pick = np.sort(rng.choice(ds.n_tasks, size=3000, replace=False))
+    exp, ess = oracle.extend_batch(ds.symbols, ds.offsets, ds.tasks[pick], ds.k,
+                                   oracle_scheme(oracle, [1, -1, -1, ds.x]), ds.band,
+                                   threads=os.cpu_count() or 1)
+    assert result_rows_equal(out.reshape(-1, 2)[pick].reshape(-1), exp).all()
+    assert (ss[pick] == ess).all()
+    serial, ss2 = xb.extend_tasks(pool, ds.tasks, ds.k, ds.band, exec_flags=4096)  # XB_FLAG_SERIAL_TAIL
+    assert result_rows_equal(serial, out).all() and (ss2 == ss).all()
