@@ -17,6 +17,7 @@
 // batches too small to fill the machine).
 #include <climits>
 #include <cstdint>
+#include <type_traits>
 #include <utility>
 
 #include "xb_kernels.cuh"
@@ -673,31 +674,42 @@ __global__ void __launch_bounds__(128) group_tier_kernel(TierParams P) {
     };
     fetch();
     it = 0;
-    while (__any_sync(0xFFFFFFFFu, active || waiting)) {
-        if (consumer && !__any_sync(0xFFFFFFFFu, active)) {  // nothing queued for this warp yet
-            __nanosleep(2000);
-            if (waiting) fetch();
+    // the consumer's polling lives in its own copy of the loop, so the
+    // ordinary launches run the loop without it
+    auto run = [&](auto cons) {
+        constexpr bool CONS = decltype(cons)::value;
+        while (__any_sync(0xFFFFFFFFu, active || (CONS && waiting))) {
+            if constexpr (CONS) {
+                if (!__any_sync(0xFFFFFFFFu, active)) {  // nothing queued for this warp yet
+                    __nanosleep(2000);
+                    if (waiting) fetch();
+                    ++it;
+                    continue;
+                }
+            }
+            if (active && (it & (St::RPER - 1)) == 0) {
+                if (lane == 0) S.rv.refill(P.pool);
+                if (lane == G - 1) S.rh.refill(P.pool);
+            }
+            const bool peel = active && !(S.d & 1);
+            if (__any_sync(0xFFFFFFFFu, peel)) {  // rare: some group resumed at an even d
+                if (peel)  // its odd half only feeds v
+                    gfeed<K, G, MODE, true, false>(S, P, S.d - 1, lane, gmask);
+                else
+                    gstep<K, G, MODE, true, false>(S, O, E, P, tab, gap, X, it, lane, gmask, sk);
+            } else {
+                gstep<K, G, MODE, true, true>(S, O, E, P, tab, gap, X, it, lane, gmask, sk);
+            }
+            gstep<K, G, MODE, false, true>(S, E, O, P, tab, gap, X, it, lane, gmask, sk);
+            // outcome recorded by the deciding step; idle consumer groups poll every 8th iteration
+            if ((active && S.stop) || (CONS && !active && waiting && (it & 7) == 0)) fetch();
             ++it;
-            continue;
         }
-        if (active && (it & (St::RPER - 1)) == 0) {
-            if (lane == 0) S.rv.refill(P.pool);
-            if (lane == G - 1) S.rh.refill(P.pool);
-        }
-        const bool peel = active && !(S.d & 1);
-        if (__any_sync(0xFFFFFFFFu, peel)) {  // rare: some group resumed at an even d
-            if (peel)  // its odd half only feeds v
-                gfeed<K, G, MODE, true, false>(S, P, S.d - 1, lane, gmask);
-            else
-                gstep<K, G, MODE, true, false>(S, O, E, P, tab, gap, X, it, lane, gmask, sk);
-        } else {
-            gstep<K, G, MODE, true, true>(S, O, E, P, tab, gap, X, it, lane, gmask, sk);
-        }
-        gstep<K, G, MODE, false, true>(S, E, O, P, tab, gap, X, it, lane, gmask, sk);
-        // outcome recorded by the deciding step; idle consumer groups poll every 8th iteration
-        if ((active && S.stop) || (!active && waiting && (it & 7) == 0)) fetch();
-        ++it;
-    }
+    };
+    if (consumer)
+        run(std::true_type{});
+    else
+        run(std::false_type{});
     if (P.pilot || lane != 0) return;
     if (sk.units) atomicAdd(&P.ctr->units[P.tier], sk.units);
     if (sk.cells) atomicAdd(&P.ctr->cells[P.tier], sk.cells);
