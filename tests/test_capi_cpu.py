@@ -85,6 +85,9 @@ def test_no_cpu_fallback():
     p = xb.DevicePool(s, b"ACGTACGT", np.array([0, 4, 8]))
     with pytest.raises(xb.xband.DeviceError, match="no CUDA device"):
         xb.extend_tasks(p, np.array([[0, 1, 0, 0]]), 2, 8)
+    # the batch stream (bench e2e) has no fallback either, and releases what it holds
+    with pytest.raises(xb.xband.DeviceError, match="no CUDA device"):
+        list(xb.xband.extend_batches([(p, np.array([[0, 1, 0, 0]]))], 2, 8))
 
 
 @pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
