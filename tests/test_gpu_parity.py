@@ -439,3 +439,48 @@ def test_config5_full_size(xb, oracle):
     assert (ss[pick] == ess).all()
     serial, ss2 = xb.extend_tasks(pool, ds.tasks, ds.k, ds.band, exec_flags=4096)  # XB_FLAG_SERIAL_TAIL
     assert result_rows_equal(serial, out).all() and (ss2 == ss).all()
+
+
+def test_edge_batches(xb, oracle):
+    """Empty batches, one-task batches, zero-length views (seeds at either end
+    of a sequence, sequences exactly k long), N in DNA (byte pool), and a
+    throughput-size batch of one repeated task: each against the oracle."""
+    s = xb.ScoringScheme.match_mismatch(1, -1, -1, 10)
+    so = oracle.scheme_mm(1, -1, -1, 10)
+    rng = np.random.default_rng(11)
+    base = "".join(rng.choice(list("ACGT"), 300))
+    seqs = [base, base[:150] + "T" + base[151:], base[:17], "AC" + base[:40], base[100:117]]
+    syms = np.frombuffer("".join(seqs).encode(), dtype=np.uint8)
+    off = np.cumsum([0] + [len(x) for x in seqs]).astype(np.int64)
+    pool = xb.DevicePool(s, syms, off)
+    k = 17
+    tasks = np.array([[0, 1, 0, 0],          # left views empty
+                      [0, 1, 283, 283],      # right views empty
+                      [2, 2, 0, 0],          # sequence exactly k long: both views empty
+                      [0, 3, 0, 2],          # left view of h empty, of v two bases
+                      [4, 0, 0, 100],        # h exactly k, seed inside v
+                      [1, 0, 150, 150]], dtype=np.int64)
+    out, ss = xb.extend_tasks(pool, tasks, k, 64)
+    exp, ess = oracle.extend_batch(syms, off, tasks, k, so, 64, threads=1)
+    assert result_rows_equal(out, exp).all() and (ss == ess).all()
+    one, s1 = xb.extend_tasks(pool, tasks[3:4], k, 64)
+    assert result_rows_equal(one, exp[6:8]).all() and s1[0] == ess[3]
+    empty, se = xb.extend_tasks(pool, tasks[:0], k, 64)
+    assert len(empty) == 0 and len(se) == 0
+    got = list(xb.xband.extend_batches([(pool, tasks[:0]), (pool, tasks)], k, 64))
+    assert len(got[0][0]) == 0 and result_rows_equal(got[1][0], exp).all()
+    # N never matches, so the pool falls back to byte codes
+    seqs_n = [base[:120] + "N" * 5 + base[125:], base]
+    sn = np.frombuffer("".join(seqs_n).encode(), dtype=np.uint8)
+    on = np.cumsum([0] + [len(x) for x in seqs_n]).astype(np.int64)
+    pn = xb.DevicePool(s, sn, on)
+    assert pn.bits_per_symbol == 8
+    tn = np.array([[0, 1, 200, 200], [1, 0, 10, 10], [0, 0, 60, 60]], dtype=np.int64)
+    o2, s2 = xb.extend_tasks(pn, tn, k, 64)
+    e2, es2 = oracle.extend_batch(sn, on, tn, k, so, 64, threads=1)
+    assert result_rows_equal(o2, e2).all() and (s2 == es2).all()
+    # one task repeated at throughput scale: every row equals the single run
+    rep = np.repeat(tasks[5:6], 60000, axis=0)
+    o3, _ = xb.extend_tasks(pool, rep, k, 64)
+    assert not xb.xband.last_stats()["start_lane_groups"]
+    assert result_rows_equal(o3, np.tile(exp[10:12], 60000)).all()
