@@ -284,7 +284,7 @@ __device__ __forceinline__ void gfinish(GState<K, G, MODE>& S, const TierParams&
 template <int K, int G, int MODE, bool ODD, bool FM>
 __device__ __forceinline__ void gstep(GState<K, G, MODE>& S, int32_t (&cur)[K / G],
                                       int32_t (&prv)[K / G], const TierParams& P,
-                                      const int8_t* __restrict__ tab, int32_t gap, int32_t X,
+                                      const tab_t* __restrict__ tab, int32_t gap, int32_t X,
                                       unsigned it, int lane, unsigned gmask, GSink& sk) {
     // the main-path shuffles use the full mask when the whole warp steps
     // together; the rare path (group-divergent) always uses the group's mask
@@ -407,7 +407,7 @@ __device__ __forceinline__ void gstep(GState<K, G, MODE>& S, int32_t (&cur)[K / 
                 case 2: asm("prmt.b32 %0, %1, %2, 0xAA62;" : "=r"(idx) : "r"(S.VWb[r]), "r"(S.HWb[r])); break;
                 default: asm("prmt.b32 %0, %1, %2, 0xBB73;" : "=r"(idx) : "r"(S.VWb[r]), "r"(S.HWb[r])); break;
             }
-            db = dg + int32_t(tab[idx]);
+            db = dg + tab[idx];
         }
         int32_t ln, un;
         if constexpr (ODD) {  // gap sources at u and u+1
@@ -489,7 +489,7 @@ __global__ void __launch_bounds__(128) group_tier_kernel(TierParams P) {
     using St = GState<K, G, MODE>;
     constexpr int SS = St::S;
     constexpr int KB = St::KB;
-    __shared__ int8_t tab[MODE == 0 ? 4 : 32 * 256];
+    __shared__ tab_t tab[MODE == 0 ? 1 : 32 * 256];  // 32 KB: word entries spread the lookups over the banks
     const int32_t gap = P.scheme->gap, X = P.scheme->x;
     const int wl = threadIdx.x & 31;
     const int lane = wl % G;
@@ -507,7 +507,7 @@ __global__ void __launch_bounds__(128) group_tier_kernel(TierParams P) {
                 val = P.scheme->sim[v * 32 + h] - 2 * gap;
                 val = max(-127, min(127, val));
             }
-            tab[i] = int8_t(val);
+            tab[i] = val;
         }
         __syncthreads();
     }

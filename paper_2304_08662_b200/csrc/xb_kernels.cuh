@@ -35,6 +35,13 @@
 namespace xb {
 
 constexpr int32_t kDeadS = -(1 << 24);  // dead sentinel in drift space
+
+// Shared score table of the table modes: tab[h*256 + v] = sim(v, h) - 2*gap,
+// one 32-bit word per entry.  Byte entries put every row of the table in
+// the same 8 of the 32 banks (h*256 is a multiple of 128 B), and protein
+// batches then ran at 7.8 shared wavefronts per lookup (ncu, C3 x10); words
+// put entry (h, v) in bank v.
+using tab_t = int32_t;
 constexpr int kTB = 128;                // threads per block, thread tiers
 constexpr int32_t kBig = 1 << 29;       // empty live range = [kBig, -kBig]
 

@@ -247,7 +247,7 @@ template <int K, int MODE, bool ODD, int k>
 __device__ __forceinline__ void slot(int32_t (&cur)[K], const int32_t (&prv)[K],
                                      const uint32_t (&Z)[(K + 15) / 16][4],
                                      const TState<K, MODE>& S, const TierParams& P,
-                                     const int8_t* __restrict__ tab, SlotCtx& X,
+                                     const tab_t* __restrict__ tab, SlotCtx& X,
                                      uint32_t (&dm)[(K + 31) / 32]) {
     const int32_t dg = cur[k];
     int32_t db;
@@ -262,7 +262,7 @@ __device__ __forceinline__ void slot(int32_t (&cur)[K], const int32_t (&prv)[K],
         uint32_t idx;
         asm("prmt.b32 %0, %1, %2, %3;"
             : "=r"(idx) : "r"(S.VW[r]), "r"(S.HW[r]), "n"(q | ((q + 4) << 4) | ((8 | q) << 8) | ((8 | q) << 12)));
-        db = imad(int32_t(tab[idx]), X.one, dg);
+        db = imad(tab[idx], X.one, dg);
     }
     int32_t ln, un;
     if constexpr (ODD) {  // gap sources at u and u+1
@@ -279,7 +279,7 @@ template <int K, int MODE, bool ODD, int... ks>
 __device__ __forceinline__ void all_slots(std::integer_sequence<int, ks...>, int32_t (&cur)[K],
                                           const int32_t (&prv)[K], const uint32_t (&Z)[(K + 15) / 16][4],
                                           const TState<K, MODE>& S, const TierParams& P,
-                                          const int8_t* __restrict__ tab, SlotCtx& X,
+                                          const tab_t* __restrict__ tab, SlotCtx& X,
                                           uint32_t (&dm)[(K + 31) / 32]) {
     // descending slot = ascending i: the order of the reference's running best
     (slot<K, MODE, ODD, K - 1 - ks>(cur, prv, Z, S, P, tab, X, dm), ...);
@@ -427,7 +427,7 @@ __device__ __forceinline__ int bfind64(uint64_t x) {
 // trigger like every other exception.
 template <int K, int MODE, bool ODD>
 __device__ __forceinline__ void xstep(TState<K, MODE>& S, int32_t (&cur)[K], int32_t (&prv)[K],
-                                      const TierParams& P, const int8_t* __restrict__ tab,
+                                      const TierParams& P, const tab_t* __restrict__ tab,
                                       int32_t gap, int32_t X, unsigned it, Sink& sk
 #if XB_COUNTERS
                                       , unsigned long long (&xb_dbg)[8]
@@ -595,7 +595,7 @@ constexpr int tier_min_blocks() {
 
 template <int K, int MODE>
 __global__ void __launch_bounds__(kTB, tier_min_blocks<K, MODE>()) thread_tier_kernel(TierParams P) {
-    __shared__ int8_t tab[MODE == 0 ? 4 : 32 * 256];
+    __shared__ tab_t tab[MODE == 0 ? 1 : 32 * 256];  // 32 KB: word entries spread the lookups over the banks
     const int32_t gap = P.scheme->gap, X = P.scheme->x;
     Queue Q;
     if (!make_queue(P, Q)) return;
@@ -608,7 +608,7 @@ __global__ void __launch_bounds__(kTB, tier_min_blocks<K, MODE>()) thread_tier_k
                 val = P.scheme->sim[v * 32 + h] - 2 * gap;
                 val = max(-127, min(127, val));
             }
-            tab[q] = int8_t(val);
+            tab[q] = val;
         }
         __syncthreads();
     }
