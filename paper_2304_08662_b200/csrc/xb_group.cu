@@ -407,7 +407,7 @@ __device__ __forceinline__ void gstep(GState<K, G, MODE>& S, int32_t (&cur)[K / 
                 case 2: asm("prmt.b32 %0, %1, %2, 0xAA62;" : "=r"(idx) : "r"(S.VWb[r]), "r"(S.HWb[r])); break;
                 default: asm("prmt.b32 %0, %1, %2, 0xBB73;" : "=r"(idx) : "r"(S.VWb[r]), "r"(S.HWb[r])); break;
             }
-            db = dg + tab[idx];
+            db = dg + tab_lookup(tab, idx);
         }
         int32_t ln, un;
         if constexpr (ODD) {  // gap sources at u and u+1
@@ -489,7 +489,7 @@ __global__ void __launch_bounds__(128) group_tier_kernel(TierParams P) {
     using St = GState<K, G, MODE>;
     constexpr int SS = St::S;
     constexpr int KB = St::KB;
-    __shared__ tab_t tab[MODE == 0 ? 1 : 32 * 256];  // 32 KB: word entries spread the lookups over the banks
+    __shared__ tab_t tab[MODE == 0 ? 1 : kTabWords];
     const int32_t gap = P.scheme->gap, X = P.scheme->x;
     const int wl = threadIdx.x & 31;
     const int lane = wl % G;
@@ -500,15 +500,7 @@ __global__ void __launch_bounds__(128) group_tier_kernel(TierParams P) {
     Queue Q;
     if (!make_queue(P, Q)) return;
     if constexpr (MODE != 0) {
-        for (int i = threadIdx.x; i < 32 * 256; i += blockDim.x) {
-            const int h = i >> 8, v = i & 255;
-            int val = -128;
-            if (v < 32 && h != kSentinel && v != kSentinel) {
-                val = P.scheme->sim[v * 32 + h] - 2 * gap;
-                val = max(-127, min(127, val));
-            }
-            tab[i] = val;
-        }
+        tab_fill(tab, P.scheme, gap);
         __syncthreads();
     }
     const int next_tier = P.esc_to_warp ? kWarpTier : P.tier + 1;

@@ -36,12 +36,32 @@ namespace xb {
 
 constexpr int32_t kDeadS = -(1 << 24);  // dead sentinel in drift space
 
-// Shared score table of the table modes: tab[h*256 + v] = sim(v, h) - 2*gap,
-// one 32-bit word per entry.  Byte entries put every row of the table in
-// the same 8 of the 32 banks (h*256 is a multiple of 128 B), and protein
-// batches then ran at 7.8 shared wavefronts per lookup (ncu, C3 x10); words
-// put entry (h, v) in bank v.
+// Shared score table of the table modes: entry (h, v) = sim(v, h) - 2*gap,
+// one 32-bit word at word index 33*h + v (codes < 32; column 32 is padding).
+// The pitch of 33 words puts entry (h, v) in bank (h + v) mod 32.  Byte
+// entries at h*256 + v had put every row in the same 8 of the 32 banks, and
+// protein batches ran at 7.8 shared wavefronts per lookup (ncu, C3 x10).
+// The byte offset 4v + 132h comes from the [v, h, 0, 0] index bytes with one
+// IDP.4A (tab_offset).
 using tab_t = int32_t;
+constexpr int kTabPitch = 33;
+constexpr int kTabWords = 32 * kTabPitch;
+__device__ __forceinline__ int32_t tab_lookup(const tab_t* __restrict__ tab, uint32_t vh_bytes) {
+    const uint32_t off = __dp4a(vh_bytes, 4u | (4u * kTabPitch) << 8, 0u);
+    return *reinterpret_cast<const tab_t*>(reinterpret_cast<const char*>(tab) + off);
+}
+// fills the table (all threads of the block, then the caller syncs)
+__device__ __forceinline__ void tab_fill(tab_t* tab, const DevScheme* scheme, int32_t gap) {
+    for (int q = threadIdx.x; q < kTabWords; q += blockDim.x) {
+        const int h = q / kTabPitch, v = q % kTabPitch;
+        int val = -128;  // sentinel rows/columns and the padding column lose
+        if (v < 32 && h != kSentinel && v != kSentinel) {
+            val = scheme->sim[v * 32 + h] - 2 * gap;
+            val = max(-127, min(127, val));
+        }
+        tab[q] = val;
+    }
+}
 constexpr int kTB = 128;                // threads per block, thread tiers
 constexpr int32_t kBig = 1 << 29;       // empty live range = [kBig, -kBig]
 

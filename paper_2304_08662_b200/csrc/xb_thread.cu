@@ -262,7 +262,7 @@ __device__ __forceinline__ void slot(int32_t (&cur)[K], const int32_t (&prv)[K],
         uint32_t idx;
         asm("prmt.b32 %0, %1, %2, %3;"
             : "=r"(idx) : "r"(S.VW[r]), "r"(S.HW[r]), "n"(q | ((q + 4) << 4) | ((8 | q) << 8) | ((8 | q) << 12)));
-        db = imad(tab[idx], X.one, dg);
+        db = imad(tab_lookup(tab, idx), X.one, dg);
     }
     int32_t ln, un;
     if constexpr (ODD) {  // gap sources at u and u+1
@@ -595,21 +595,12 @@ constexpr int tier_min_blocks() {
 
 template <int K, int MODE>
 __global__ void __launch_bounds__(kTB, tier_min_blocks<K, MODE>()) thread_tier_kernel(TierParams P) {
-    __shared__ tab_t tab[MODE == 0 ? 1 : 32 * 256];  // 32 KB: word entries spread the lookups over the banks
+    __shared__ tab_t tab[MODE == 0 ? 1 : kTabWords];
     const int32_t gap = P.scheme->gap, X = P.scheme->x;
     Queue Q;
     if (!make_queue(P, Q)) return;
     if constexpr (MODE != 0) {
-        // tab[h*256 + v] = sim(v, h) - 2*gap; sentinel rows/cols lose
-        for (int q = threadIdx.x; q < 32 * 256; q += blockDim.x) {
-            const int h = q >> 8, v = q & 255;
-            int val = -128;
-            if (v < 32 && h != kSentinel && v != kSentinel) {
-                val = P.scheme->sim[v * 32 + h] - 2 * gap;
-                val = max(-127, min(127, val));
-            }
-            tab[q] = val;
-        }
+        tab_fill(tab, P.scheme, gap);
         __syncthreads();
     }
     const int next_tier = P.esc_to_warp ? kWarpTier : P.tier + 1;
