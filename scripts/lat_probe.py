@@ -55,7 +55,7 @@ def main():
                 "t0": FORCE | NO_GROUP | (0 << 8), "t1": FORCE | NO_GROUP | (1 << 8),
                 "t2": FORCE | NO_GROUP | (2 << 8), "t3": FORCE | NO_GROUP | (3 << 8),
                 "t4": FORCE | NO_GROUP | (4 << 8),
-                "g1": FORCE | GROUP | (1 << 8), "g2": FORCE | GROUP | (2 << 8), "g3": FORCE | GROUP | (3 << 8)}
+                "g0": FORCE | GROUP | (0 << 8), "g1": FORCE | GROUP | (1 << 8), "g2": FORCE | GROUP | (2 << 8), "g3": FORCE | GROUP | (3 << 8)}
     for cfg in [int(c) for c in a.configs.split(",")]:
         ds = synth.make(cfg, 1.0)
         if cfg == 3:
