@@ -656,9 +656,18 @@ __global__ void __launch_bounds__(128) group_tier_kernel(TierParams P) {
                     E[s] = odd ? vp : vc;
                 }
                 S.d = odd ? d : d - 1;
-                g_windows(S, P.pool, lane, r, r);
+                // a record written at an even d: its odd half-iteration only feeds
+                // v, its even step runs here (readers set up with a full refill
+                // period, as this happens before the next refill point), and the
+                // group joins the loop at an odd d, so the loop itself never peels
+                g_windows(S, P.pool, lane, odd ? r : St::RPER - 1, odd ? r : St::RPER - 1);
                 S.d = d;
                 g_limits(S);
+                if (!odd) {
+                    gfeed<K, G, MODE, true, false>(S, P, d - 1, lane, gmask);
+                    gstep<K, G, MODE, false, false>(S, E, O, P, tab, gap, X, it, lane, gmask, sk);
+                    if (!S.stop) g_windows(S, P.pool, lane, r, r);  // the loop's refill schedule
+                }
             }
             active = true;
             return;
@@ -683,15 +692,9 @@ __global__ void __launch_bounds__(128) group_tier_kernel(TierParams P) {
                 if (lane == 0) S.rv.refill(P.pool);
                 if (lane == G - 1) S.rh.refill(P.pool);
             }
-            const bool peel = active && !(S.d & 1);
-            if (__any_sync(0xFFFFFFFFu, peel)) {  // rare: some group resumed at an even d
-                if (peel)  // its odd half only feeds v
-                    gfeed<K, G, MODE, true, false>(S, P, S.d - 1, lane, gmask);
-                else
-                    gstep<K, G, MODE, true, false>(S, O, E, P, tab, gap, X, it, lane, gmask, sk);
-            } else {
-                gstep<K, G, MODE, true, true>(S, O, E, P, tab, gap, X, it, lane, gmask, sk);
-            }
+            // every group steps on odd d here (fetch() runs the even step of a
+            // unit resumed at an even d), so the warp needs no peeled half
+            gstep<K, G, MODE, true, true>(S, O, E, P, tab, gap, X, it, lane, gmask, sk);
             gstep<K, G, MODE, false, true>(S, E, O, P, tab, gap, X, it, lane, gmask, sk);
             // outcome recorded by the deciding step; idle consumer groups poll every 8th iteration
             if ((active && S.stop) || (CONS && !active && waiting && (it & 7) == 0)) fetch();
