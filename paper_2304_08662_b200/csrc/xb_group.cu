@@ -432,11 +432,13 @@ __device__ __forceinline__ void gstep(GState<K, G, MODE>& S, int32_t (&cur)[K / 
         int32_t Mj[G];
 #pragma unroll
         for (int j = 0; j < G; ++j) Mj[j] = __shfl_sync(smask, Mk, j, G);
-#pragma unroll
-        for (int j = 0; j < G; ++j) {
-            all = max(all, Mj[j]);
-            if (j > lane) above = max(above, Mj[j]);
-        }
+        // lane-constant offsets (0 for higher lanes, -2^29 otherwise: keys are
+        // below 2^29 by the drift-range guard, so a masked key minus C stays
+        // below Tc > 0) instead of a select chain
+        static_assert(G == 4, "written for G = 4");
+        above = __vimax3_s32(Mj[1] + (lane < 1 ? 0 : -(1 << 29)), Mj[2] + (lane < 2 ? 0 : -(1 << 29)),
+                             Mj[3] + (lane < 3 ? 0 : -(1 << 29)));
+        all = __vimax3_s32(Mj[0], Mj[1], max(Mj[2], Mj[3]));
     }
     int32_t c = __viaddmax_s32(above, negC, S.Tc);
     // pass 3: lane-local chain, drop test, dead mask (lane-relative keys)
