@@ -525,6 +525,7 @@ __global__ void __launch_bounds__(128) group_tier_kernel(TierParams P) {
     // (table modes index the shared table with those codes): start them empty
     S.rv.cur = S.rh.cur = 0u;
     S.rv.w0 = S.rv.w1 = S.rh.w0 = S.rh.w1 = 0u;
+    S.rv.pend = S.rh.pend = 0u;
     S.rv.sh = S.rh.sh = 0u;
 #pragma unroll
     for (int r = 0; r < St::NB; ++r) S.VWb[r] = S.HWb[r] = 0u;
@@ -544,7 +545,7 @@ __global__ void __launch_bounds__(128) group_tier_kernel(TierParams P) {
     // did, the consumer leaves everything to the kRoleEscalations launch.
     const unsigned long long t_start = consumer ? globaltimer_ns() : 0ull;
     unsigned it = 0xFFFFFFFFu;
-    auto fetch = [&]() {
+    auto fetch = [&]() __attribute__((always_inline)) {
         active = false;
         for (;;) {
             unsigned long long i = 0;

@@ -176,11 +176,16 @@ __device__ __forceinline__ uint32_t chunk_mem_e(const uint32_t* __restrict__ poo
 // symbols needed up to the next refill point, and each refill assembles the
 // chunk whose words were loaded one refill earlier.  TOP = chunks top-first
 // (v side: consume from the top field), else bottom-first (h side).
-template <bool TOP, int ENC = ENC_2BIT>
+// PF: hold one more word (`pend`), loaded a whole refill period before it is
+// first read, so no refill waits on a load; without it, the word loaded at a
+// refill is consumed right there (one register fewer, for the K <= 24 thread
+// tiers whose register budget is exhausted).
+template <bool TOP, int ENC = ENC_2BIT, bool PF = true>
 struct Reader {
     using F = EncFields<ENC>;
     uint32_t cur;   // remaining symbols until the next refill point
     uint32_t w0, w1;
+    uint32_t pend;  // PF: the word after them
     int64_t wnext;  // word index of the next load
     uint32_t sh;
     int32_t dir;
@@ -200,17 +205,30 @@ struct Reader {
         sh = uint32_t(q & (F::PER - 1)) * uint32_t(F::BITS);
         w0 = ldw(pool, wi);
         w1 = ldw(pool, wi + 1);
-        wnext = d ? wi + 2 : wi - 1;
+        if constexpr (PF) {
+            pend = ldw(pool, d ? wi + 2 : wi - 1);
+            wnext = d ? wi + 3 : wi - 2;
+        } else {
+            wnext = d ? wi + 2 : wi - 1;
+        }
     }
     __device__ __forceinline__ void refill(const uint32_t* pool) {
         const uint32_t c = __funnelshift_r(w0, w1, sh);
         const bool rev = TOP ? (dir != 0) : (dir == 0);
         cur = rev ? rev_fields<ENC>(c) : c;
-        const uint32_t nw = ldw(pool, wnext);
         const bool fwd = dir != 0;
         const uint32_t o0 = w0, o1 = w1;
-        w0 = fwd ? o1 : nw;
-        w1 = fwd ? nw : o0;
+        if constexpr (PF) {
+            // the word loaded at the previous refill slides in; the load issued
+            // now is first read a whole refill period later (no scoreboard wait)
+            w0 = fwd ? o1 : pend;
+            w1 = fwd ? pend : o0;
+            pend = ldw(pool, wnext);
+        } else {
+            const uint32_t nw = ldw(pool, wnext);
+            w0 = fwd ? o1 : nw;
+            w1 = fwd ? nw : o0;
+        }
         wnext += fwd ? 1 : -1;
     }
     // the next symbol's code (v side: TOP, h side: !TOP)
@@ -253,8 +271,9 @@ struct TState {
     uint32_t HW[MODE == 0 ? NW : NB];
     static constexpr int RENC = MODE == 2 ? ENC_8BIT : ENC_2BIT;  // pool encoding read
     static constexpr int RPER = EncFields<RENC>::PER;              // refill period (iterations)
-    Reader<true, RENC> rv;
-    Reader<false, RENC> rh;
+    static constexpr bool RPF = K >= 32 && MODE == 0;  // register headroom for the prefetched word
+    Reader<true, RENC, RPF> rv;
+    Reader<false, RENC, RPF> rh;
 };
 
 // LR split + seed score + cost keys, one thread per task
