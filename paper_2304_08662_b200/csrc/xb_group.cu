@@ -302,6 +302,64 @@ __device__ __forceinline__ void gstep(GState<K, G, MODE>& S, int32_t (&cur)[K / 
     int wm1 = s_hi + M - KB;
     uint32_t vml = gbits(0, SS - 1);  // this lane's in-matrix slots
     [[maybe_unused]] uint32_t inv = 0u;
+    const int32_t negC = -((X << 6) + 63);
+    int32_t cand[SS], key[SS];
+    // Table modes: pass 1 runs speculatively on the current state, beside the
+    // rare-path test that the previous step's live-range gather feeds; a
+    // group that takes the rare path (which may shift the band or mark the
+    // matrix edge) redoes it after.  (Measured: C3 3.61 -> 3.40 ms.  The same
+    // reordering made the 2-bit DNA step slower under load, C2 6.63 -> 6.77
+    // ms, so that mode keeps pass 1 after the rare path.)
+    [[maybe_unused]] auto tpass1 = [&](unsigned msk) __attribute__((always_inline)) {
+        // gap source across the lane edge
+        int32_t edge;
+        if constexpr (ODD) {
+            edge = __shfl_down_sync(msk, prv[0], 1, G);
+            if (lane == G - 1) edge = kDeadS;
+        } else {
+            edge = __shfl_up_sync(msk, prv[SS - 1], 1, G);
+            if (lane == 0) edge = kDeadS;
+        }
+        // match bytes (see the thread tier): byte j of Z[q] = 1 + 2*match of slot 4j+q
+        [[maybe_unused]] uint32_t Z[4];
+        if constexpr (MODE == 0) {
+            const uint32_t x = glop3<0xBE>(S.VW, S.HW, inv);  // (a ^ b) | c
+            const uint32_t z = ~(x | (x << 1));
+    #pragma unroll
+            for (int q = 0; q < 4; ++q) Z[q] = ((z >> (2 * q)) & 0x02020202u) | 0x01010101u;
+        }
+
+        // pass 1: candidates and keys (key' = 64 cand + s, lane-relative)
+    #pragma unroll
+        for (int s = SS - 1; s >= 0; --s) {
+            const int32_t dg = cur[s];
+            int32_t db;
+            if constexpr (MODE == 0) {
+                db = __dp4a(int(Z[s & 3]), 1 << (8 * ((s >> 2) & 3)), dg);
+            } else {
+                const int r = s >> 2, q = s & 3;
+                uint32_t idx = 0;
+                switch (q) {  // bytes: v code, h code, 0, 0
+                    case 0: asm("prmt.b32 %0, %1, %2, 0x8840;" : "=r"(idx) : "r"(S.VWb[r]), "r"(S.HWb[r])); break;
+                    case 1: asm("prmt.b32 %0, %1, %2, 0x9951;" : "=r"(idx) : "r"(S.VWb[r]), "r"(S.HWb[r])); break;
+                    case 2: asm("prmt.b32 %0, %1, %2, 0xAA62;" : "=r"(idx) : "r"(S.VWb[r]), "r"(S.HWb[r])); break;
+                    default: asm("prmt.b32 %0, %1, %2, 0xBB73;" : "=r"(idx) : "r"(S.VWb[r]), "r"(S.HWb[r])); break;
+                }
+                db = dg + tab_lookup(tab, idx);
+            }
+            int32_t ln, un;
+            if constexpr (ODD) {  // gap sources at u and u+1
+                ln = prv[s];
+                un = s < SS - 1 ? prv[s < SS - 1 ? s + 1 : s] : edge;
+            } else {              // gap sources at u-1 and u
+                ln = s > 0 ? prv[s > 0 ? s - 1 : s] : edge;
+                un = prv[s];
+            }
+            cand[s] = __vimax3_s32(db, ln, un);
+            key[s] = cand[s] * 64 + s;
+        }
+    };
+    if constexpr (MODE != 0) tpass1(smask);
     // group-uniform rare path
     if ((M > KB || unsigned(s_hi) > unsigned(K - 1) || unsigned(wm1) >= unsigned(P.band) ||
          d >= S.d_lim) && !S.stop) {
@@ -367,58 +425,59 @@ __device__ __forceinline__ void gstep(GState<K, G, MODE>& S, int32_t (&cur)[K / 
                 wm1 = max(w, 0) - 1;
             }
         }
+        if constexpr (MODE != 0) tpass1(gmask);
     }
     S.cells += wm1 + 1;
     S.delta_w = max(S.delta_w, wm1 + 1);
 
-    // gap source across the lane edge
-    int32_t edge;
-    if constexpr (ODD) {
-        edge = __shfl_down_sync(smask, prv[0], 1, G);
-        if (lane == G - 1) edge = kDeadS;
-    } else {
-        edge = __shfl_up_sync(smask, prv[SS - 1], 1, G);
-        if (lane == 0) edge = kDeadS;
-    }
-    // match bytes (see the thread tier): byte j of Z[q] = 1 + 2*match of slot 4j+q
-    [[maybe_unused]] uint32_t Z[4];
     if constexpr (MODE == 0) {
-        const uint32_t x = glop3<0xBE>(S.VW, S.HW, inv);  // (a ^ b) | c
-        const uint32_t z = ~(x | (x << 1));
-#pragma unroll
-        for (int q = 0; q < 4; ++q) Z[q] = ((z >> (2 * q)) & 0x02020202u) | 0x01010101u;
-    }
-
-    const int32_t negC = -((X << 6) + 63);
-    // pass 1: candidates and keys (key' = 64 cand + s, lane-relative)
-    int32_t cand[SS], key[SS];
-#pragma unroll
-    for (int s = SS - 1; s >= 0; --s) {
-        const int32_t dg = cur[s];
-        int32_t db;
-        if constexpr (MODE == 0) {
-            db = __dp4a(int(Z[s & 3]), 1 << (8 * ((s >> 2) & 3)), dg);
+        // gap source across the lane edge
+        int32_t edge;
+        if constexpr (ODD) {
+            edge = __shfl_down_sync(smask, prv[0], 1, G);
+            if (lane == G - 1) edge = kDeadS;
         } else {
-            const int r = s >> 2, q = s & 3;
-            uint32_t idx = 0;
-            switch (q) {  // bytes: v code, h code, 0, 0
-                case 0: asm("prmt.b32 %0, %1, %2, 0x8840;" : "=r"(idx) : "r"(S.VWb[r]), "r"(S.HWb[r])); break;
-                case 1: asm("prmt.b32 %0, %1, %2, 0x9951;" : "=r"(idx) : "r"(S.VWb[r]), "r"(S.HWb[r])); break;
-                case 2: asm("prmt.b32 %0, %1, %2, 0xAA62;" : "=r"(idx) : "r"(S.VWb[r]), "r"(S.HWb[r])); break;
-                default: asm("prmt.b32 %0, %1, %2, 0xBB73;" : "=r"(idx) : "r"(S.VWb[r]), "r"(S.HWb[r])); break;
+            edge = __shfl_up_sync(smask, prv[SS - 1], 1, G);
+            if (lane == 0) edge = kDeadS;
+        }
+        // match bytes (see the thread tier): byte j of Z[q] = 1 + 2*match of slot 4j+q
+        [[maybe_unused]] uint32_t Z[4];
+        if constexpr (MODE == 0) {
+            const uint32_t x = glop3<0xBE>(S.VW, S.HW, inv);  // (a ^ b) | c
+            const uint32_t z = ~(x | (x << 1));
+    #pragma unroll
+            for (int q = 0; q < 4; ++q) Z[q] = ((z >> (2 * q)) & 0x02020202u) | 0x01010101u;
+        }
+
+        // pass 1: candidates and keys (key' = 64 cand + s, lane-relative)
+    #pragma unroll
+        for (int s = SS - 1; s >= 0; --s) {
+            const int32_t dg = cur[s];
+            int32_t db;
+            if constexpr (MODE == 0) {
+                db = __dp4a(int(Z[s & 3]), 1 << (8 * ((s >> 2) & 3)), dg);
+            } else {
+                const int r = s >> 2, q = s & 3;
+                uint32_t idx = 0;
+                switch (q) {  // bytes: v code, h code, 0, 0
+                    case 0: asm("prmt.b32 %0, %1, %2, 0x8840;" : "=r"(idx) : "r"(S.VWb[r]), "r"(S.HWb[r])); break;
+                    case 1: asm("prmt.b32 %0, %1, %2, 0x9951;" : "=r"(idx) : "r"(S.VWb[r]), "r"(S.HWb[r])); break;
+                    case 2: asm("prmt.b32 %0, %1, %2, 0xAA62;" : "=r"(idx) : "r"(S.VWb[r]), "r"(S.HWb[r])); break;
+                    default: asm("prmt.b32 %0, %1, %2, 0xBB73;" : "=r"(idx) : "r"(S.VWb[r]), "r"(S.HWb[r])); break;
+                }
+                db = dg + tab_lookup(tab, idx);
             }
-            db = dg + tab_lookup(tab, idx);
+            int32_t ln, un;
+            if constexpr (ODD) {  // gap sources at u and u+1
+                ln = prv[s];
+                un = s < SS - 1 ? prv[s < SS - 1 ? s + 1 : s] : edge;
+            } else {              // gap sources at u-1 and u
+                ln = s > 0 ? prv[s > 0 ? s - 1 : s] : edge;
+                un = prv[s];
+            }
+            cand[s] = __vimax3_s32(db, ln, un);
+            key[s] = cand[s] * 64 + s;
         }
-        int32_t ln, un;
-        if constexpr (ODD) {  // gap sources at u and u+1
-            ln = prv[s];
-            un = s < SS - 1 ? prv[s < SS - 1 ? s + 1 : s] : edge;
-        } else {              // gap sources at u-1 and u
-            ln = s > 0 ? prv[s > 0 ? s - 1 : s] : edge;
-            un = prv[s];
-        }
-        cand[s] = __vimax3_s32(db, ln, un);
-        key[s] = cand[s] * 64 + s;
     }
     // pass 2: one all-gather round of the lane maxima gives every lane the
     // maximum over the higher lanes (its chain input) and the group maximum
