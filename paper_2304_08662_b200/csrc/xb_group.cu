@@ -741,6 +741,27 @@ __global__ void __launch_bounds__(128) group_tier_kernel(TierParams P) {
     // ordinary launches run the loop without it
     auto run = [&](auto cons) {
         constexpr bool CONS = decltype(cons)::value;
+        if constexpr (!CONS) {
+            // the steps run in an inner loop that fetch() is not part of: it
+            // exits (one vote per iteration, as the loop test was) when some
+            // group's unit is decided, so the back edge carries no merge with
+            // fetch()'s writes
+            while (__any_sync(0xFFFFFFFFu, active)) {
+                for (;;) {
+                    if (active && (it & (St::RPER - 1)) == 0) {
+                        if (lane == 0) S.rv.refill(P.pool);
+                        if (lane == G - 1) S.rh.refill(P.pool);
+                    }
+                    gstep<K, G, MODE, true, true>(S, O, E, P, tab, gap, X, it, lane, gmask, sk);
+                    gstep<K, G, MODE, false, true>(S, E, O, P, tab, gap, X, it, lane, gmask, sk);
+                    if (__any_sync(0xFFFFFFFFu, active && S.stop)) break;
+                    ++it;
+                }
+                if (active && S.stop) fetch();
+                ++it;
+            }
+            return;
+        }
         while (__any_sync(0xFFFFFFFFu, active || (CONS && waiting))) {
             if constexpr (CONS) {
                 if (!__any_sync(0xFFFFFFFFu, active)) {  // nothing queued for this warp yet
