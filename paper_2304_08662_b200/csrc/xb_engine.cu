@@ -1037,13 +1037,15 @@ __global__ void gather_patch_kernel(TierParams P, int t0, uint32_t* __restrict__
 
 // Resident lane-group blocks per SM for a latency-bound start tier.  A block
 // puts one warp (8 groups) on each SMSP.  A lone warp advances one step per
-// ~380 cycles of latency while issuing ~170 instructions, so a second warp per
+// ~490 cycles of latency while issuing ~160 instructions, so a second warp per
 // SMSP fits in the latency shadow and a third only slows every step down --
 // including the longest unit's, which sets the batch's wall time.  Batches
 // that fit one block per SM keep one warp per SMSP: spreading the units over
 // more SMSPs shortens every step.  Measured on 1 B200 (scripts/lat_sweep.sh,
-// tier ms at 4/3/2/1 blocks): C1 0.57/0.45/0.35/0.31, C2 10.6/8.8/7.4/12.6,
-// C3 4.97/4.98/4.98/5.52.
+// tier ms at 4/3/2/1 blocks, first version): C1 0.57/0.45/0.35/0.31,
+// C2 10.6/8.8/7.4/12.6, C3 4.97/4.98/4.98/5.52; after the step-loop changes
+// (batch ms at 3/2/1 blocks): C1 0.50/0.40/0.36, C2 8.13/6.49/11.7,
+// C3 3.18/3.17/4.46 (2 for C2 and C3, 1 for C1: the engine's choice).
 // Lane-group blocks that consume the next tier's escalations while a
 // throughput start tier runs.  Each one displaces about one start-tier block
 // (1/592 of the machine); 4 blocks serve 128 escalated units at a time, which

@@ -30,7 +30,7 @@ import paper_2304_08662_b200 as xb  # noqa: E402
 from paper_2304_08662_b200 import capi, synth  # noqa: E402
 
 OPS_PER_CELL = 8
-GROUP_STEP_CYCLES = 380  # lone K32 lane group, ncu
+GROUP_STEP_CYCLES = 490  # lone K32 DNA lane group, measured
 
 
 def cpu_model() -> str:
