@@ -1088,7 +1088,10 @@ static int run_cascade(xb_batch* B, DevBatch& D) {
             if (D.all_group || D.no_group) {
                 tp.role = kRoleAll;
                 int per_sm = D.all_group ? D.gocc[t] : D.occ[t];
-                if (D.all_group && t == D.t0) per_sm = std::min(per_sm, latency_blocks_per_sm(D));
+                // latency mode: the escalation tiers after the start tier get no more
+                // resident blocks than it (their work is the start tier's long units;
+                // a full-occupancy grid of mostly idle blocks only costs launch time)
+                if (D.all_group && t >= D.t0) per_sm = std::min(per_sm, latency_blocks_per_sm(D));
                 CK(launch_tier(D.all_group, mode, t, tp, D.sm_count * per_sm, D.stream));
                 ++D.launches;
             } else if (t == D.t0) {  // the start tier: one thread per unit
