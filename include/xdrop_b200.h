@@ -102,7 +102,8 @@ typedef struct {
     int64_t h2d_bytes, d2h_bytes;
     int32_t sm_count;
     int32_t start_tier;          /* tier the pilot chose */
-    int64_t dbg[6];              /* instrumented builds only (-DXB_COUNTERS=1), else 0 */
+    int64_t dbg[6];              /* [0..4] instrumented builds only (-DXB_COUNTERS=1), else 0;
+                                    [5] units a lane-group tier resumed at an even antidiagonal */
     int32_t start_lane_groups;   /* 1: the start tier ran as lane groups (latency-bound batch) */
     int32_t reserved;
 } xb_stats;

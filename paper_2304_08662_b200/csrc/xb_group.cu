@@ -726,6 +726,7 @@ __global__ void __launch_bounds__(128) group_tier_kernel(TierParams P) {
                 S.d = d;
                 g_limits(S);
                 if (!odd) {
+                    if (lane == 0) atomicAdd(&P.ctr->dbg[5], 1ull);  // stats: even-d resumes
                     gfeed<K, G, MODE, true, false>(S, P, d - 1, lane, gmask);
                     gstep<K, G, MODE, false, false>(S, E, O, P, tab, gap, X, it, lane, gmask, sk);
                     if (!S.stop) g_windows(S, P.pool, lane, r, r);  // the loop's refill schedule

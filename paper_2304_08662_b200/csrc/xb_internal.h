@@ -55,7 +55,8 @@ struct DevCounters {
     unsigned long long units[8];
     unsigned long long cells[8];
     unsigned long long escalated[8];
-    unsigned long long dbg[8];         // XB_COUNTERS builds: steps, rare, masked, recenters, stops
+    unsigned long long dbg[8];         // XB_COUNTERS builds: steps, rare, masked, recenters, stops;
+                                       // [5] always: lane-group resumes at an even d
     int32_t start_tier;                // chosen by the pilot
     int32_t pad;
     unsigned long long resume_next;    // resume records handed out

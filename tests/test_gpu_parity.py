@@ -236,6 +236,7 @@ def test_band_failures_and_escalation(xb, oracle, flags):
             if rng.random() < 0.25:
                 v[q] = rng.choice(b"ACGT")
         entries.append((h, bytes(v)))
+    even_resumes = 0
     for x, band in ((60, 1000), (120, 1000), (60, 70), (30, 40)):
         so = oracle.scheme_mm(1, -1, -1, x)
         sym = b"".join(h + v for h, v in entries)
@@ -248,8 +249,13 @@ def test_band_failures_and_escalation(xb, oracle, flags):
             units[q] = (2 * q, 2 * q + 1, 1, 1, 0, 0, len(h), len(v))
         pool = xb.DevicePool(xb.ScoringScheme.match_mismatch(1, -1, -1, x), sym, np.array(off))
         out = xb.extend_units(pool, units, band, exec_flags=flags)
+        even_resumes += xb.xband.last_stats()["dbg"][5]
         for q, (h, v) in enumerate(entries):
             assert rec_tuple(out[q]) == rec_tuple(oracle.extend(h, v, so, band)), (x, band, q)
+    if flags == 32 | 8:
+        # lane-group tiers from K16 up: records written at even antidiagonals
+        # take the first-step-in-fetch() path, and it was exercised here
+        assert even_resumes > 0
 
 
 def test_pipeline_drop_in(xb):
