@@ -240,21 +240,26 @@ struct DevPool {
     int64_t* seq_pos = nullptr;
     int64_t* seq_len = nullptr;
     DevScheme* scheme = nullptr;
+    int64_t cap_words = 0, cap_seqs = 0;  // allocated sizes (the pool may grow after an upload)
     bool ready = false;
 };
 
 struct Workspace;
 
+// The detached pool (SequenceStore, sequence.hpp:13-19) keeps no byte copy of
+// its sequences: xb_pool_add* validates the symbols and packs them straight
+// into one pinned host image of 32-bit words (2-bit DNA, or one byte code per
+// symbol), which is what crosses PCIe once per device.  The image grows in
+// place; a DNA pool that receives its first 'N' is widened from 2-bit to byte
+// codes once (ACGTN codes are 0-4 in both, so the widening is a re-layout).
 struct xb_pool {
     xb_scheme scheme;
-    std::vector<char> symbols;
-    std::vector<int64_t> offsets{0};
-    bool all_acgt = true;
-    // packed host image
-    bool packed = false;
+    std::vector<int64_t> offsets{0};  // symbol offsets of the sequences (no padding)
     int enc = ENC_2BIT;
-    uint32_t* host_words = nullptr;  // pinned
-    int64_t n_words = 0;
+    uint32_t* host_words = nullptr;   // pinned when host_pinned
+    bool host_pinned = false;
+    int64_t cap_words = 0;            // allocated words of host_words
+    int64_t n_words = 0;              // words covering pad + symbols + pad (+2)
     std::vector<int64_t> seq_pos, seq_len;
     DevScheme dev_scheme{};
     std::map<int, DevPool> dev;
@@ -278,50 +283,47 @@ static bool thread_tiers_ok(const xb_pool* p) {
     return true;
 }
 
-static void pool_pack(xb_pool* p) {
-    if (p->packed) return;
-    const xb_scheme& s = p->scheme;
-    p->enc = (s.kind == 0 && p->all_acgt) ? ENC_2BIT : ENC_8BIT;
-    const int64_t total = int64_t(p->symbols.size());
-    const int64_t nsym = kPoolPad + total + kPoolPad;
-    p->n_words = p->enc == ENC_2BIT ? (nsym + 15) / 16 + 2 : (nsym + 3) / 4 + 2;
-    if (p->host_words) cudaFreeHost(p->host_words);
-    if (cudaMallocHost(&p->host_words, size_t(p->n_words) * 4) != cudaSuccess) {
+static int enc_per(int enc) { return enc == ENC_2BIT ? 16 : 4; }
+static int enc_bits(int enc) { return enc == ENC_2BIT ? 2 : 8; }
+static int64_t words_for(int enc, int64_t total) {
+    return (kPoolPad + total + kPoolPad + enc_per(enc) - 1) / enc_per(enc) + 2;
+}
+
+static void host_free(uint32_t* w, bool pinned) {
+    if (!w) return;
+    if (pinned)
+        cudaFreeHost(w);
+    else
+        std::free(w);
+}
+
+// A zeroed image of at least `need` words (pinned when the runtime allows),
+// holding the first `keep` words of the old one.
+static bool host_reserve(xb_pool* p, int64_t need, int64_t keep) {
+    if (need <= p->cap_words) return true;
+    const int64_t cap = std::max<int64_t>(need, p->cap_words + p->cap_words / 2);
+    uint32_t* w = nullptr;
+    bool pinned = cudaMallocHost(&w, size_t(cap) * 4) == cudaSuccess;
+    if (!pinned) {
         cudaGetLastError();
-        p->host_words = (uint32_t*)std::malloc(size_t(p->n_words) * 4);
+        w = static_cast<uint32_t*>(std::malloc(size_t(cap) * 4));
+        if (!w) return false;
     }
-    uint8_t code[256];
-    for (int c = 0; c < 256; ++c) code[c] = 0;
-    if (p->enc == ENC_2BIT) {
-        code['A'] = 0;
-        code['C'] = 1;
-        code['G'] = 2;
-        code['T'] = 3;
-    } else {
-        for (int c = 0; c < 256; ++c) code[c] = s.code_of[c] < 0 ? 0 : uint8_t(s.code_of[c]);
-    }
-    const char* sym = p->symbols.data();
-    uint32_t* W = p->host_words;
-    const int per = p->enc == ENC_2BIT ? 16 : 4;
-    const int bits = p->enc == ENC_2BIT ? 2 : 8;
-    parallel_for(p->n_words, [&](int64_t a, int64_t b) {
-        for (int64_t w = a; w < b; ++w) {
-            uint32_t acc = 0;
-            const int64_t p0 = w * per;
-            for (int q = 0; q < per; ++q) {
-                const int64_t s0 = p0 + q - kPoolPad;
-                if (s0 >= 0 && s0 < total) acc |= uint32_t(code[(unsigned char)sym[s0]]) << (bits * q);
-            }
-            W[w] = acc;
-        }
+    parallel_for(cap, [&](int64_t a, int64_t b) {
+        const int64_t c = std::min(b, keep);
+        if (a < c) std::memcpy(w + a, p->host_words + a, size_t(c - a) * 4);
+        if (std::max(a, c) < b) std::memset(w + std::max(a, c), 0, size_t(b - std::max(a, c)) * 4);
     });
-    const int64_t n = int64_t(p->offsets.size()) - 1;
-    p->seq_pos.resize(size_t(n));
-    p->seq_len.resize(size_t(n));
-    for (int64_t i = 0; i < n; ++i) {
-        p->seq_pos[size_t(i)] = kPoolPad + p->offsets[size_t(i)];
-        p->seq_len[size_t(i)] = p->offsets[size_t(i) + 1] - p->offsets[size_t(i)];
-    }
+    host_free(p->host_words, p->host_pinned);
+    p->host_words = w;
+    p->host_pinned = pinned;
+    p->cap_words = cap;
+    return true;
+}
+
+// Kernel-side scheme: code-pair table, encoding, guards.
+static void pool_scheme(xb_pool* p) {
+    const xb_scheme& s = p->scheme;
     DevScheme& d = p->dev_scheme;
     std::memset(&d, 0, sizeof d);
     d.gap = s.gap;
@@ -347,22 +349,65 @@ static void pool_pack(xb_pool* p) {
         d.max_score = std::max(d.max_score, v);
         d.min_score = std::min(d.min_score, v);
     }
-    p->packed = true;
+}
+
+// 2-bit image -> byte codes (A0 C1 G2 T3 are the ACGTN scheme's codes too).
+static bool widen_to_bytes(xb_pool* p) {
+    const int64_t total = p->offsets.back();
+    const int64_t nw = words_for(ENC_8BIT, total);
+    uint32_t* w = nullptr;
+    bool pinned = cudaMallocHost(&w, size_t(nw) * 4) == cudaSuccess;
+    if (!pinned) {
+        cudaGetLastError();
+        w = static_cast<uint32_t*>(std::malloc(size_t(nw) * 4));
+        if (!w) return false;
+    }
+    const uint32_t* old = p->host_words;
+    parallel_for(nw, [&](int64_t a, int64_t b) {
+        for (int64_t q = a; q < b; ++q) {
+            uint32_t acc = 0;
+            for (int f = 0; f < 4; ++f) {
+                const int64_t s = 4 * q + f;  // symbol position (pad included)
+                const uint32_t c = (old[s >> 4] >> (2 * (s & 15))) & 3u;
+                acc |= c << (8 * f);
+            }
+            w[q] = acc;
+        }
+    });
+    host_free(p->host_words, p->host_pinned);
+    p->host_words = w;
+    p->host_pinned = pinned;
+    p->cap_words = nw;
+    p->n_words = nw;
+    p->enc = ENC_8BIT;
+    return true;
 }
 
 static int pool_device(xb_pool* p, int dev, cudaStream_t st, int64_t* h2d, DevPool** out) {
     std::lock_guard<std::mutex> g(p->mu);
-    pool_pack(p);
     DevPool& D = p->dev[dev];
     if (!D.ready) {
         CK(cudaSetDevice(dev));
         const int64_t n = int64_t(p->seq_pos.size());
+        // A pool that grew after an upload (more sequences, or an 'N' that
+        // switched it from 2-bit to byte codes) outgrows its device buffers:
+        // reallocate.  cudaFree waits for the device to go idle, so no batch
+        // still reading the old buffers is cut short.
+        if (D.words && (p->n_words > D.cap_words || n > D.cap_seqs)) {
+            CK(cudaFree(D.words));
+            CK(cudaFree(D.seq_pos));
+            CK(cudaFree(D.seq_len));
+            D.words = nullptr;
+            D.seq_pos = D.seq_len = nullptr;
+        }
         if (!D.words) {
             CK(cudaMalloc(&D.words, size_t(p->n_words) * 4));
             CK(cudaMalloc(&D.seq_pos, size_t(std::max<int64_t>(n, 1)) * 8));
             CK(cudaMalloc(&D.seq_len, size_t(std::max<int64_t>(n, 1)) * 8));
-            CK(cudaMalloc(&D.scheme, sizeof(DevScheme)));
+            D.cap_words = p->n_words;
+            D.cap_seqs = std::max<int64_t>(n, 1);
         }
+        if (!D.scheme) CK(cudaMalloc(&D.scheme, sizeof(DevScheme)));
         CK(cudaMemcpyAsync(D.words, p->host_words, size_t(p->n_words) * 4, cudaMemcpyHostToDevice, st));
         if (n) {
             CK(cudaMemcpyAsync(D.seq_pos, p->seq_pos.data(), size_t(n) * 8, cudaMemcpyHostToDevice, st));
@@ -370,8 +415,8 @@ static int pool_device(xb_pool* p, int dev, cudaStream_t st, int64_t* h2d, DevPo
         }
         CK(cudaMemcpyAsync(D.scheme, &p->dev_scheme, sizeof(DevScheme), cudaMemcpyHostToDevice, st));
         // the pinned words stream over PCIe while the host stages the tasks;
-        // batch creation waits for the stream before returning, so the pool
-        // cannot be repacked under an in-flight copy
+        // batch creation waits for the stream before returning, so the image
+        // cannot be grown under an in-flight copy
         if (h2d) *h2d += p->n_words * 4 + n * 16 + int64_t(sizeof(DevScheme));
         D.ready = true;
     }
@@ -400,6 +445,14 @@ xb_pool* xb_pool_create(const xb_scheme* s, int* err) {
     }
     auto* p = new xb_pool();
     p->scheme = *s;
+    p->enc = s->kind == 0 ? ENC_2BIT : ENC_8BIT;
+    if (!host_reserve(p, words_for(p->enc, 0), 0)) {
+        delete p;
+        if (err) *err = XB_E_BAD_PARAM;
+        return nullptr;
+    }
+    p->n_words = words_for(p->enc, 0);
+    pool_scheme(p);
     if (err) *err = XB_OK;
     return p;
 }
@@ -425,13 +478,36 @@ int64_t xb_pool_add_bulk(xb_pool* p, const char* concat, const int64_t* offsets,
     });
     if (bad) return -XB_E_UNKNOWN_SYMBOL;
     std::lock_guard<std::mutex> g(p->mu);
+    if (non_acgt && p->enc == ENC_2BIT && !widen_to_bytes(p)) return -XB_E_BAD_PARAM;
     const int64_t first = int64_t(p->offsets.size()) - 1;
-    const int64_t at = int64_t(p->symbols.size());
-    p->symbols.resize(size_t(at + total));
-    std::memcpy(p->symbols.data() + at, base, size_t(total));
-    for (int64_t i = 0; i < n; ++i) p->offsets.push_back(at + offsets[i + 1] - offsets[0]);
-    if (non_acgt) p->all_acgt = false;
-    p->packed = false;
+    const int64_t at = p->offsets.back();
+    const int64_t nw = words_for(p->enc, at + total);
+    if (!host_reserve(p, nw, p->n_words)) return -XB_E_BAD_PARAM;
+    // pack the new symbols into the words they fall in; the image past the
+    // old symbols is zero, so a word shared with them is OR-ed into
+    uint8_t code[256];
+    for (int c = 0; c < 256; ++c) code[c] = p->scheme.code_of[c] < 0 ? 0 : uint8_t(p->scheme.code_of[c]);
+    const int per = enc_per(p->enc), bits = enc_bits(p->enc);
+    const int64_t s0 = kPoolPad + at, s1 = s0 + total;  // image symbol positions of the new run
+    uint32_t* W = p->host_words;
+    parallel_for((s1 - s0 + per - 1) / per + 1, [&](int64_t a, int64_t b) {
+        for (int64_t q = s0 / per + a; q < s0 / per + b; ++q) {
+            const int64_t lo = std::max(q * per, s0), hi = std::min(q * per + per, s1);
+            if (lo >= hi) continue;
+            uint32_t acc = 0;
+            for (int64_t s = lo; s < hi; ++s)
+                acc |= uint32_t(code[(unsigned char)base[s - s0]]) << (bits * int(s - q * per));
+            W[q] |= acc;
+        }
+    });
+    p->n_words = nw;
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t o0 = at + offsets[i] - offsets[0], o1 = at + offsets[i + 1] - offsets[0];
+        p->offsets.push_back(o1);
+        p->seq_pos.push_back(kPoolPad + o0);
+        p->seq_len.push_back(o1 - o0);
+    }
+    pool_scheme(p);
     for (auto& kv : p->dev) kv.second.ready = false;
     return first;
 }
@@ -448,9 +524,7 @@ int64_t xb_pool_seq_len(const xb_pool* p, int64_t id) {
     return p->offsets[size_t(id) + 1] - p->offsets[size_t(id)];
 }
 
-int xb_pool_bits_per_symbol(const xb_pool* p) {
-    return (p->scheme.kind == 0 && p->all_acgt) ? 2 : 8;
-}
+int xb_pool_bits_per_symbol(const xb_pool* p) { return enc_bits(p->enc); }
 
 void xb_pool_evict(xb_pool* p) {
     std::lock_guard<std::mutex> g(p->mu);
@@ -460,7 +534,7 @@ void xb_pool_evict(xb_pool* p) {
 void xb_pool_free(xb_pool* p) {
     if (!p) return;
     pool_drop_devices(p);
-    if (p->host_words) cudaFreeHost(p->host_words);
+    host_free(p->host_words, p->host_pinned);
     delete p;
 }
 
@@ -760,14 +834,15 @@ static int setup_device(xb_batch* B, DevBatch& D, const xb_exec* ex) {
         CK(cudaMallocHost(&W.h_tasks, size_t(I) * 32));
         W.capI = I;
     }
-    // warp-tier scratch: 2*band ints per resident warp, capped at 1 GiB
+    // warp-tier scratch: 2*band ints per warp slot, capped at 1 GiB (down to
+    // a single warp when one warp's rows alone are that large)
     {
         const int64_t per_warp = 2LL * B->band * 4;
         // one warp slot per unit at most: a small batch with a huge band (the
         // band survey: band = L + 1) needs kilobytes, not the full 16 per SM
-        int64_t warps = std::min<int64_t>(int64_t(D.sm_count) * 16, std::max<int64_t>(D.n_units, 4));
-        warps = std::min<int64_t>(warps, std::max<int64_t>(4, (1LL << 30) / per_warp));
-        warps = (warps + 3) / 4 * 4;
+        int64_t warps = std::min<int64_t>(int64_t(D.sm_count) * 16, std::max<int64_t>(D.n_units, 1));
+        warps = std::min<int64_t>(warps, std::max<int64_t>(1, (1LL << 30) / per_warp));
+        if (warps > 4) warps = (warps + 3) / 4 * 4;
         D.scratch_warps = int(warps);
         const size_t need = size_t(warps * per_warp);
         if (need > W.scratch_bytes) {
@@ -1139,11 +1214,13 @@ static int run_cascade(xb_batch* B, DevBatch& D) {
     // ---- warp per unit: exact generic path for whatever is left ----
     {
         tp.tier = kWarpTier;
-        const int blocks = D.scratch_warps / 4;
+        // one warp per scratch slot: blocks of 4 warps, or one smaller block
+        const int wpb = std::min(4, D.scratch_warps);
+        const int blocks = D.scratch_warps / wpb;
         if (p->enc == ENC_2BIT)
-            warp_tier_kernel<ENC_2BIT><<<blocks, 128, 0, D.stream>>>(tp);
+            warp_tier_kernel<ENC_2BIT><<<blocks, 32 * wpb, 0, D.stream>>>(tp);
         else
-            warp_tier_kernel<ENC_8BIT><<<blocks, 128, 0, D.stream>>>(tp);
+            warp_tier_kernel<ENC_8BIT><<<blocks, 32 * wpb, 0, D.stream>>>(tp);
         CK(cudaGetLastError());
         ++D.launches;
     }
@@ -1218,6 +1295,7 @@ static int validate_tasks(const xb_pool* p, const xb_task* tasks, int64_t n, int
     const int64_t chunk = (n + T - 1) / std::max(T, 1);
     std::vector<int64_t> first_dangling(size_t(std::max(T, 1)), INT64_MAX);
     std::vector<int64_t> first_oob(size_t(std::max(T, 1)), INT64_MAX);
+    std::vector<int64_t> first_long(size_t(std::max(T, 1)), INT64_MAX);  // a view of 2^31+ symbols
     auto scan = [&](int c) {
         const int64_t a = c * chunk, b = std::min(n, a + chunk);
         for (int64_t t = a; t < b; ++t) {
@@ -1232,6 +1310,10 @@ static int validate_tasks(const xb_pool* p, const xb_task* tasks, int64_t n, int
             if (int64_t(q.h_seed) + k > hl || int64_t(q.v_seed) + k > vl ||
                 q.h_seed > uint64_t(hl) || q.v_seed > uint64_t(vl))
                 first_oob[size_t(c)] = t;
+            else if (first_long[size_t(c)] == INT64_MAX &&
+                     (int64_t(q.h_seed) > kMaxViewLen || int64_t(q.v_seed) > kMaxViewLen ||
+                      hl - int64_t(q.h_seed) - k > kMaxViewLen || vl - int64_t(q.v_seed) - k > kMaxViewLen))
+                first_long[size_t(c)] = t;
         }
     };
     if (T <= 1) {
@@ -1251,6 +1333,11 @@ static int validate_tasks(const xb_pool* p, const xb_task* tasks, int64_t n, int
         if (bad) *bad = ob;
         return XB_E_SEED_OOB;
     }
+    const int64_t lg = *std::min_element(first_long.begin(), first_long.end());
+    if (lg != INT64_MAX) {
+        if (bad) *bad = lg;
+        return XB_E_OUT_OF_RANGE;
+    }
     return XB_OK;
 }
 
@@ -1264,6 +1351,7 @@ xb_batch* xb_batch_create(xb_pool* p, const xb_task* tasks, int64_t n, int k, in
         return nullptr;
     };
     if (!p || n < 0 || k < 0 || band < 1 || (n && !tasks)) return fail(XB_E_BAD_PARAM, nullptr);
+    std::unique_lock<std::mutex> lk(p->mu);  // the pool must not grow under the scans
     int rc = validate_tasks(p, tasks, n, k, bad_task);
     if (rc) return fail(rc, nullptr);
     std::vector<int> ids;
@@ -1289,6 +1377,7 @@ xb_batch* xb_batch_create(xb_pool* p, const xb_task* tasks, int64_t n, int k, in
         shard_lpt(cost, int(ids.size()), sh);
         for (size_t g = 0; g < ids.size(); ++g) B->devs[g].tasks = std::move(sh[g]);
     }
+    lk.unlock();
     for (size_t g = 0; g < ids.size(); ++g) {
         DevBatch& D = B->devs[g];
         D.dev = ids[g];
@@ -1469,10 +1558,7 @@ int xb_extend_batch(xb_pool* p, const xb_task* tasks, int64_t n, int k, int band
 int xb_extend_units(xb_pool* p, const xb_unit* units, int64_t n, int band, xb_side_result* out,
                     int64_t* bad_unit, const xb_exec* exec) {
     if (!p || n < 0 || band < 1 || (n && !units)) return XB_E_BAD_PARAM;
-    {
-        std::lock_guard<std::mutex> g(p->mu);
-        pool_pack(p);
-    }
+    std::unique_lock<std::mutex> lk(p->mu);  // the pool must not grow under the scan
     const int64_t ns = xb_pool_size(p);
     std::vector<DevUnit> all(static_cast<size_t>(n));
     for (int64_t q = 0; q < n; ++q) {
@@ -1488,7 +1574,10 @@ int xb_extend_units(xb_pool* p, const xb_unit* units, int64_t n, int band, xb_si
             const uint64_t room = dir ? uint64_t(len) - origin : origin;
             return length > room;
         };
-        if (bad_view(hn, u.h_origin, u.h_dir, u.h_len) || bad_view(vn, u.v_origin, u.v_dir, u.v_len)) {
+        // views of 2^31 symbols or more: the result fields (int h_ext/v_ext,
+        // align.hpp:37-45) and the kernels' int32 lengths cannot hold them
+        if (bad_view(hn, u.h_origin, u.h_dir, u.h_len) || bad_view(vn, u.v_origin, u.v_dir, u.v_len) ||
+            u.h_len > uint64_t(kMaxViewLen) || u.v_len > uint64_t(kMaxViewLen)) {
             if (bad_unit) *bad_unit = q;
             return XB_E_OUT_OF_RANGE;
         }
@@ -1504,6 +1593,7 @@ int xb_extend_units(xb_pool* p, const xb_unit* units, int64_t n, int band, xb_si
                                 p->scheme.x + 2;
         d.route = (bound < (1LL << 23) && u.h_len < (1ull << 30) && u.v_len < (1ull << 30)) ? 0 : 2;
     }
+    lk.unlock();
     std::vector<int> ids;
     int rc = exec_devices(exec, ids);
     if (rc) return rc;

@@ -14,6 +14,11 @@ enum : int { ENC_2BIT = 2, ENC_8BIT = 8 };
 // fetches that run past a sequence (masked out later) never leave the buffer
 constexpr int64_t kPoolPad = 4096;
 
+// Longest view (extension length) a batch accepts: the result fields are int
+// (ExtensionResult, align.hpp:37-45) and the kernels keep lengths in int32.
+// Longer views are rejected with XB_E_OUT_OF_RANGE.
+constexpr int64_t kMaxViewLen = 0x7FFFFFFF;
+
 // Code reserved for "outside the view": scores -128 (+2gap drift) in the
 // thread tier's table, so out-of-matrix diagonals always lose.
 constexpr int kSentinel = 31;

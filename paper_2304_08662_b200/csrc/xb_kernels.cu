@@ -27,8 +27,8 @@ __device__ __forceinline__ uint32_t bit_range(int lo, int hi) {
 constexpr int32_t kDeadW = INT_MIN;
 
 template <int ENC>
-__device__ __forceinline__ int slot_of(int k, int i, int band) {
-    int u = (k - i) % band;
+__device__ __forceinline__ int slot_of(long long k, int i, int band) {
+    int u = int((k - i) % band);
     return u < 0 ? u + band : u;
 }
 
@@ -57,14 +57,17 @@ __global__ void __launch_bounds__(128) warp_tier_kernel(TierParams P) {
         const int m = U.h_len, n = U.v_len;
 
         int32_t* R[2] = {rows0, rows1};
-        int rk[2] = {0, 0}, rfl[2] = {0, 0}, rll[2] = {0, -1};
+        long long rk[2] = {0, 0};
+        int rfl[2] = {0, 0}, rll[2] = {0, -1};
         if (lane == 0) rows0[0] = 0;  // slot_of(0, 0) = 0
         __syncwarp();
         int32_t T = 0;
-        int best_d = 0, best_i = 0, delta_w = 1, status = kStatusOk, spread = 0;
+        long long best_d = 0;
+        int best_i = 0, delta_w = 1, status = kStatusOk, spread = 0;
         long long cells = 1;
 
-        for (int d = 1; d <= n + m + 1; ++d) {
+        // 64-bit antidiagonals: views up to kMaxViewLen each
+        for (long long d = 1; d <= (long long)n + m + 1; ++d) {
             const int ci = d & 1, pi = ci ^ 1;
             int32_t* cur = R[ci];
             const int32_t* prev = R[pi];
@@ -81,8 +84,8 @@ __global__ void __launch_bounds__(128) warp_tier_kernel(TierParams P) {
                 hi = max(hi, (long long)rll[ci] + 1);
             }
             lo = max(lo, (long long)(d > m ? d - m : 0));
-            hi = min(hi, (long long)min(d, n));
-            const int kn = d / 2;
+            hi = min(hi, min(d, (long long)n));
+            const long long kn = d / 2;
             if (lo > hi) {
                 rk[ci] = kn;
                 rfl[ci] = 0;
@@ -106,7 +109,7 @@ __global__ void __launch_bounds__(128) warp_tier_kernel(TierParams P) {
                 int32_t val = kDeadW;
                 int sg = 0;
                 if (act) {
-                    const int j = d - i;
+                    const int j = int(d - i);
                     sg = slot_of<ENC>(kn, i, band);
                     if (i - 1 >= pp_fl && i - 1 <= pp_ll) {
                         const int32_t dg = cur[sg];
@@ -167,7 +170,7 @@ __global__ void __launch_bounds__(128) warp_tier_kernel(TierParams P) {
                 res.score = res.h_ext = res.v_ext = 0;
             } else {
                 res.score = T;
-                res.h_ext = best_d - best_i;
+                res.h_ext = int(best_d - best_i);
                 res.v_ext = best_i;
             }
             res.delta_w = delta_w;

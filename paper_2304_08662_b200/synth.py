@@ -4,28 +4,17 @@ tasks (n, 4) int64 = (h_id, v_id, h_seed, v_seed)."""
 from __future__ import annotations
 
 import ctypes as C
-import json
-import os
 from dataclasses import dataclass
 
 import numpy as np
 
+from . import blosum62
 from .capi import check, lib
-
-HERE = os.path.dirname(os.path.abspath(__file__))
-BLOSUM62_JSON = os.path.join(os.path.dirname(HERE), "tests", "golden", "blosum62.json")
 
 
 def blosum62_text() -> str:
-    """NCBI-format BLOSUM62 text rebuilt from the committed fixture."""
-    with open(BLOSUM62_JSON) as f:
-        m = json.load(f)
-    alpha, cells = m["alphabet"], m["cells"]
-    n = len(alpha)
-    lines = ["   " + "  ".join(alpha)]
-    for i, a in enumerate(alpha):
-        lines.append(a + " " + " ".join(f"{cells[i * n + j]:2d}" for j in range(n)))
-    return "\n".join(lines) + "\n"
+    """NCBI-format BLOSUM62 text (the package constant, blosum62.py)."""
+    return blosum62.text()
 
 
 @dataclass

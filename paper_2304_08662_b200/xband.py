@@ -300,6 +300,17 @@ class DevicePool:
         np.cumsum([len(s.symbols) for s in store], out=off[1:])
         return DevicePool(scheme, data, off)
 
+    def add(self, symbols: bytes | str) -> int:
+        """Appends one sequence (SequenceStore push_back); returns its id.
+        A pool may grow after it was uploaded: the next batch re-uploads it."""
+        b = symbols.encode() if isinstance(symbols, str) else bytes(symbols)
+        buf = C.create_string_buffer(b, len(b) + 1)
+        r = lib().xb_pool_add(self._h, buf, len(b))
+        if r < 0:
+            _raise(int(-r), "xb_pool_add")
+        self.n += 1
+        return int(r)
+
     @property
     def bits_per_symbol(self) -> int:
         return lib().xb_pool_bits_per_symbol(self._h)

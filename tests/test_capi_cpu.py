@@ -143,3 +143,34 @@ def test_sweep_band_validation_precedes_device():
     with pytest.raises(xb.InputError):
         xb.sweep_band(10, [5], [0.9])  # 17-mer seed longer than the pair
     assert xb.sweep_band(100, [], [0.9]) == "x\terror_rate\tdelta_w\n"
+
+
+def test_pool_packs_incrementally():
+    """The pool keeps only the packed image: 2-bit while every sequence is
+    ACGT, byte codes from the first N on; ids are dense across adds."""
+    import paper_2304_08662_b200 as xb
+    s = xb.ScoringScheme.match_mismatch(1, -1, -1, 5)
+    p = xb.DevicePool(s, b"ACGT", np.array([0, 2, 4], dtype=np.int64))
+    assert p.bits_per_symbol == 2
+    assert p.add("ACGTACGT" * 1000) == 2
+    assert p.bits_per_symbol == 2
+    assert p.add("ACNGT") == 3
+    assert p.bits_per_symbol == 8
+    assert p.add("T") == 4
+    assert xb.capi.lib().xb_pool_size(p._h) == 5
+    assert xb.capi.lib().xb_pool_seq_len(p._h, 3) == 5
+    with pytest.raises(xb.UnknownSymbol):
+        p.add("ACGX")
+    m = xb.ScoringScheme.from_matrix(xb.SubMatrix("AB", [2, -1, -1, 3]), -1, 4)
+    q = xb.DevicePool(m, b"ABBA", np.array([0, 4], dtype=np.int64))
+    assert q.bits_per_symbol == 8
+
+
+def test_package_blosum62_matches_reference_fixture():
+    """The package's BLOSUM62 constant equals the reference's parse of
+    proj/data/BLOSUM62 (tests/golden/blosum62.json, made by the reference)."""
+    from paper_2304_08662_b200 import blosum62 as B
+    a, c = blosum62()
+    assert B.ALPHABET == a and list(B.CELLS) == list(c)
+    m = xb.parse_submatrix(B.text())
+    assert m.alphabet == a and list(m.cells) == list(c)

@@ -490,3 +490,52 @@ def test_edge_batches(xb, oracle):
     o3, _ = xb.extend_tasks(pool, rep, k, 64)
     assert not xb.xband.last_stats()["start_lane_groups"]
     assert result_rows_equal(o3, np.tile(exp[10:12], 60000)).all()
+
+
+def test_pool_grows_after_upload(xb, oracle):
+    """A pool used by a batch, then grown (more sequences; then an 'N' that
+    widens it from 2-bit to byte codes), then used again: every batch equals
+    the oracle over the pool's contents at that point (the device copy is
+    reallocated when the packed image outgrows it)."""
+    rng = random.Random(77)
+
+    def rnd(n, alpha="ACGT"):
+        return "".join(rng.choice(alpha) for _ in range(n))
+
+    scheme = xb.ScoringScheme.match_mismatch(1, -1, -1, 12)
+    pool = xb.DevicePool(scheme, b"", np.zeros(1, dtype=np.int64))
+    seqs = []
+
+    def grow(count, alpha="ACGT"):
+        for _ in range(count):
+            base = rnd(rng.randint(300, 3000), alpha)
+            seqs.append(base)
+            assert pool.add(base) == len(seqs) - 1
+
+    def check():
+        sym = "".join(seqs).encode()
+        off = np.zeros(len(seqs) + 1, dtype=np.int64)
+        np.cumsum([len(s) for s in seqs], out=off[1:])
+        tasks = []
+        for _ in range(400):
+            h, v = rng.randrange(len(seqs)), rng.randrange(len(seqs))
+            hs = rng.randrange(len(seqs[h]) - 17)
+            vs = rng.randrange(len(seqs[v]) - 17)
+            tasks.append((h, v, hs, vs))
+        t = np.array(tasks, dtype=np.int64)
+        out, ss = xb.extend_tasks(pool, t, 17, 256)
+        exp, ess = oracle.extend_batch(np.frombuffer(sym, np.uint8), off, t, 17,
+                                       oracle.scheme_mm(1, -1, -1, 12), 256)
+        assert result_rows_equal(out, exp).all()
+        assert (ss == ess).all()
+
+    grow(20)
+    assert pool.bits_per_symbol == 2
+    check()
+    grow(300)                 # far more words than the first upload held
+    check()
+    grow(5, "ACGTN")          # first N: the image widens to byte codes (4x the words)
+    assert pool.bits_per_symbol == 8
+    check()
+    grow(50)
+    check()
