@@ -8,7 +8,7 @@ CSRC := paper_2304_08662_b200/csrc
 LIB := paper_2304_08662_b200/_lib/libxdrop_b200.so
 OBJDIR := build
 
-SRCS_CU := $(CSRC)/xb_kernels.cu $(CSRC)/xb_thread.cu $(CSRC)/xb_group.cu $(CSRC)/xb_engine.cu
+SRCS_CU := $(CSRC)/xb_kernels.cu $(CSRC)/xb_thread.cu $(CSRC)/xb_group.cu $(CSRC)/xb_wide.cu $(CSRC)/xb_engine.cu
 SRCS_CPP := $(CSRC)/xb_synth.cpp $(CSRC)/xb_ingest.cpp
 HDRS := $(CSRC)/xb_internal.h $(CSRC)/xb_kernels.cuh include/xdrop_b200.h
 
@@ -30,6 +30,10 @@ $(OBJDIR)/xb_group.o: $(CSRC)/xb_group.cu $(HDRS)
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(NVFLAGS) -dc -o $@ $< 2> $(OBJDIR)/xb_group.ptxas.txt || (cat $(OBJDIR)/xb_group.ptxas.txt; exit 1)
 
+$(OBJDIR)/xb_wide.o: $(CSRC)/xb_wide.cu $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -dc -o $@ $< 2> $(OBJDIR)/xb_wide.ptxas.txt || (cat $(OBJDIR)/xb_wide.ptxas.txt; exit 1)
+
 $(OBJDIR)/xb_engine.o: $(CSRC)/xb_engine.cu $(HDRS)
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(NVFLAGS) -dc -o $@ $< 2> $(OBJDIR)/xb_engine.ptxas.txt || (cat $(OBJDIR)/xb_engine.ptxas.txt; exit 1)
@@ -42,7 +46,7 @@ $(OBJDIR)/xb_ingest.o: $(CSRC)/xb_ingest.cpp include/xdrop_b200.h
 	@mkdir -p $(OBJDIR)
 	/usr/bin/g++ -O3 -std=c++17 -fPIC -Wall -c -o $@ $<
 
-$(LIB): $(OBJDIR)/xb_kernels.o $(OBJDIR)/xb_thread.o $(OBJDIR)/xb_group.o $(OBJDIR)/xb_engine.o $(OBJDIR)/xb_synth.o $(OBJDIR)/xb_ingest.o
+$(LIB): $(OBJDIR)/xb_kernels.o $(OBJDIR)/xb_thread.o $(OBJDIR)/xb_group.o $(OBJDIR)/xb_wide.o $(OBJDIR)/xb_engine.o $(OBJDIR)/xb_synth.o $(OBJDIR)/xb_ingest.o
 	@mkdir -p $(dir $(LIB))
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^ -lpthread
 

@@ -85,20 +85,24 @@ typedef struct {
 #define XB_FLAG_NO_GROUP 64     /* never use lane groups: one thread per unit throughout (ablation) */
 #define XB_FLAG_THROUGHPUT 128  /* plan a small batch like a large one: pilot + cost model (testing) */
 #define XB_FLAG_SERIAL_TAIL 4096 /* wider tiers only after the start tier (no concurrent escalation consumer; ablation) */
+#define XB_FLAG_LOCALITY 8192   /* multi-device batches: locality-aware shards (xb_shard_tasks XB_SHARD_LOCALITY) */
 
 /* Per-call device statistics (summed over devices; times are the max).
- * Tiers: 0..4 = one unit per thread with a K = 16/24/32/48/64 slot band,
- * 5 = one warp per unit (exact generic path). */
+ * Tiers: 0..4 = one unit per thread (or per 4-lane group) with a
+ * K = 16/24/32/48/64 slot register band; 5..8 = one warp per unit with a
+ * K = 128/256/512/1024 slot register band; 9 = one warp per unit, rows in
+ * global memory (exact generic path, any band). */
+#define XB_NUM_TIERS 10
 typedef struct {
     int32_t n_devices;
     int32_t launches;            /* kernels launched by the last run */
     double ms_total;             /* device time of the whole run */
     double ms_prep;              /* LR split + seed scores + cost sort */
     double ms_pilot;             /* pilot sample + start-tier choice */
-    double ms_tier[6];
-    int64_t units_tier[6];       /* units finished per tier */
-    int64_t cells_tier[6];       /* sum of ExtensionResult.cells finished per tier */
-    int64_t escalated[6];        /* units handed from tier t to tier t+1 */
+    double ms_tier[XB_NUM_TIERS];
+    int64_t units_tier[XB_NUM_TIERS];  /* units finished per tier */
+    int64_t cells_tier[XB_NUM_TIERS];  /* sum of ExtensionResult.cells finished per tier */
+    int64_t escalated[XB_NUM_TIERS];   /* units handed from tier t to tier t+1 */
     int64_t h2d_bytes, d2h_bytes;
     int32_t sm_count;
     int32_t start_tier;          /* tier the pilot chose */
@@ -169,6 +173,23 @@ int xb_batch_sync(xb_batch* b);
 int xb_batch_fetch(xb_batch* b, xb_side_result* out, int32_t* seed_score);
 int xb_batch_stats(xb_batch* b, xb_stats* st);
 void xb_batch_free(xb_batch* b);
+
+/* ---- sharding across processes / devices (partition.cpp:110-305) ---- */
+/* Splits a task list into n_shards (one per GPU: torchrun ranks, or the
+ * devices of one xb_exec): shard_of[t] in [0, n_shards), deterministic.
+ * XB_SHARD_LPT: longest-processing-time on the estimated task cost (the
+ *   assignment xb_extend_batch uses across devices; schedule_batches,
+ *   partition.cpp:231-305, without the tile-memory test).
+ * XB_SHARD_LOCALITY: tasks ordered along a breadth-first sweep of the
+ *   sequence graph and cut into contiguous runs of equal cost, so each shard
+ *   references a compact part of the pool (the reference's graph partition,
+ *   partition.cpp:110-184, re-targeted from IPU tiles to GPUs); a device then
+ *   uploads only the sequences its shard references.
+ * Validation and error codes as xb_extend_batch. */
+#define XB_SHARD_LPT 0
+#define XB_SHARD_LOCALITY 1
+int xb_shard_tasks(xb_pool* p, const xb_task* tasks, int64_t n, int k, int n_shards, int mode,
+                   int32_t* shard_of, int64_t* bad_task);
 
 /* stats of the last xb_extend_batch / xb_extend_units call on this thread */
 int xb_last_stats(xb_stats* st);

@@ -36,6 +36,10 @@ XB_FLAG_GROUP = 32
 XB_FLAG_NO_GROUP = 64
 XB_FLAG_THROUGHPUT = 128
 XB_FLAG_SERIAL_TAIL = 4096
+XB_FLAG_LOCALITY = 8192
+
+XB_SHARD_LPT = 0
+XB_SHARD_LOCALITY = 1
 
 
 def force_tier(t: int) -> int:
@@ -58,8 +62,13 @@ class XbExec(C.Structure):
                 ("stream", C.c_void_p), ("flags", C.c_int32)]
 
 
-TIER_NAMES = ["thread_k16", "thread_k24", "thread_k32", "thread_k48", "thread_k64", "warp"]
-TIER_WIDTHS = [16, 24, 32, 48, 64]
+# tiers 0-4: thread / lane-group register bands; 5-8: wide (one warp per unit); 9: warp tier
+TIER_NAMES = ["thread_k16", "thread_k24", "thread_k32", "thread_k48", "thread_k64",
+              "wide_k128", "wide_k256", "wide_k512", "wide_k1024", "warp"]
+TIER_WIDTHS = [16, 24, 32, 48, 64, 128, 256, 512, 1024]
+NUM_TIERS = len(TIER_NAMES)
+WIDE_FIRST = 5
+WARP_TIER = 9
 
 
 def tier_kernel_name(t: int, stats: dict, flags: int = 0) -> str:
@@ -68,6 +77,8 @@ def tier_kernel_name(t: int, stats: dict, flags: int = 0) -> str:
     their escalations on lane groups (xb_engine.cu, run_cascade)."""
     if t >= len(TIER_WIDTHS):
         return "warp"
+    if t >= WIDE_FIRST:
+        return f"wide_k{TIER_WIDTHS[t]}"
     s = stats.get("start_tier", -1)
     group = bool(flags & 32) or (t == s and stats.get("start_lane_groups")) or (t > s >= 0 and not flags & 64)
     return f"{'group' if group else 'thread'}_k{TIER_WIDTHS[t]}"
@@ -75,9 +86,9 @@ def tier_kernel_name(t: int, stats: dict, flags: int = 0) -> str:
 
 class XbStats(C.Structure):
     _fields_ = [("n_devices", C.c_int32), ("launches", C.c_int32), ("ms_total", C.c_double),
-                ("ms_prep", C.c_double), ("ms_pilot", C.c_double), ("ms_tier", C.c_double * 6),
-                ("units_tier", C.c_int64 * 6), ("cells_tier", C.c_int64 * 6),
-                ("escalated", C.c_int64 * 6), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
+                ("ms_prep", C.c_double), ("ms_pilot", C.c_double),
+                ("ms_tier", C.c_double * NUM_TIERS), ("units_tier", C.c_int64 * NUM_TIERS),
+                ("cells_tier", C.c_int64 * NUM_TIERS), ("escalated", C.c_int64 * NUM_TIERS), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
                 ("sm_count", C.c_int32), ("start_tier", C.c_int32), ("dbg", C.c_int64 * 6),
                 ("start_lane_groups", C.c_int32), ("reserved", C.c_int32)]
 
@@ -129,6 +140,7 @@ def lib() -> C.CDLL:
         "xb_batch_stats": (I, [P, C.POINTER(XbStats)]),
         "xb_batch_free": (V, [P]),
         "xb_last_stats": (I, [C.POINTER(XbStats)]),
+        "xb_shard_tasks": (I, [P, P, I64, I, I, I, P, C.POINTER(I64)]),
         "xb_measure_int32_peak": (I, [I, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                       C.POINTER(C.c_double), C.POINTER(I)]),
         "xb_synth_make": (P, [I, C.c_double, C.c_uint64, C.c_char_p, I, C.POINTER(I)]),
@@ -165,7 +177,7 @@ EXPORTED = ["xb_version", "xb_strerror", "xb_device_count", "xb_scheme_match_mis
             "xb_last_stats", "xb_measure_int32_peak", "xb_synth_make", "xb_synth_sizes",
             "xb_synth_copy", "xb_synth_free", "xb_synth_pairs", "xb_sweep_band", "xb_fasta_parse",
             "xb_fasta_sizes", "xb_fasta_copy", "xb_pool_add_fasta", "xb_fasta_free", "xb_parse_seeds",
-            "xb_parse_overlaps"]
+            "xb_parse_overlaps", "xb_shard_tasks"]
 
 
 class XbParseError(C.Structure):

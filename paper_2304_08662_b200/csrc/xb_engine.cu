@@ -30,6 +30,8 @@ template <int K, int MODE>
 __global__ void thread_tier_kernel(TierParams P);
 template <int K, int G, int MODE>
 __global__ void group_tier_kernel(TierParams P);
+template <int K, int MODE>
+__global__ void wide_tier_kernel(TierParams P);
 template <int ENC>
 __global__ void warp_tier_kernel(TierParams P);
 __global__ void select_tier_kernel(TierParams P, int forced, int32_t* host_out);
@@ -235,13 +237,23 @@ void xb_scheme_free(xb_scheme* s) { delete s; }
 
 // ------------------------------------------------------------------- pool ----
 
+// One device's copy of the pool.  Sequences become resident on first use:
+// a batch uploads the words of the sequences it references that this device
+// does not hold yet (or the whole image when that is most of it), so every
+// sequence crosses PCIe once per device however many seeds share it, and a
+// device serving one shard of the tasks holds only that shard's part.
 struct DevPool {
     uint32_t* words = nullptr;
     int64_t* seq_pos = nullptr;
     int64_t* seq_len = nullptr;
     DevScheme* scheme = nullptr;
     int64_t cap_words = 0, cap_seqs = 0;  // allocated sizes (the pool may grow after an upload)
-    bool ready = false;
+    bool ready = false;                   // the whole image is resident
+    bool meta_ready = false;              // seq_pos / seq_len / scheme are current
+    std::vector<uint8_t> resident;        // per sequence (when !ready)
+    uint32_t* d_stage = nullptr;          // gathered words of a partial upload
+    int64_t* d_ranges = nullptr;          // (dst word, src word, words) triples
+    int64_t cap_stage = 0, cap_ranges = 0;
 };
 
 struct Workspace;
@@ -383,12 +395,23 @@ static bool widen_to_bytes(xb_pool* p) {
     return true;
 }
 
-static int pool_device(xb_pool* p, int dev, cudaStream_t st, int64_t* h2d, DevPool** out) {
+__global__ void scatter_words_kernel(const uint32_t* __restrict__ src, const int64_t* __restrict__ ranges,
+                                     int64_t n_ranges, uint32_t* __restrict__ dst) {
+    for (int64_t r = blockIdx.x; r < n_ranges; r += gridDim.x) {
+        const int64_t d0 = ranges[3 * r], s0 = ranges[3 * r + 1], len = ranges[3 * r + 2];
+        for (int64_t q = threadIdx.x; q < len; q += blockDim.x) dst[d0 + q] = src[s0 + q];
+    }
+}
+
+// Makes the pool resident on `dev` for a batch referencing the sequences in
+// `need` (nullptr: all of them).  The caller's stream orders the copies.
+static int pool_device(xb_pool* p, int dev, cudaStream_t st, int64_t* h2d, DevPool** out,
+                       const std::vector<uint8_t>* need = nullptr) {
     std::lock_guard<std::mutex> g(p->mu);
     DevPool& D = p->dev[dev];
+    CK(cudaSetDevice(dev));
+    const int64_t n = int64_t(p->seq_pos.size());
     if (!D.ready) {
-        CK(cudaSetDevice(dev));
-        const int64_t n = int64_t(p->seq_pos.size());
         // A pool that grew after an upload (more sequences, or an 'N' that
         // switched it from 2-bit to byte codes) outgrows its device buffers:
         // reallocate.  cudaFree waits for the device to go idle, so no batch
@@ -399,6 +422,7 @@ static int pool_device(xb_pool* p, int dev, cudaStream_t st, int64_t* h2d, DevPo
             CK(cudaFree(D.seq_len));
             D.words = nullptr;
             D.seq_pos = D.seq_len = nullptr;
+            D.resident.clear();
         }
         if (!D.words) {
             CK(cudaMalloc(&D.words, size_t(p->n_words) * 4));
@@ -408,17 +432,84 @@ static int pool_device(xb_pool* p, int dev, cudaStream_t st, int64_t* h2d, DevPo
             D.cap_seqs = std::max<int64_t>(n, 1);
         }
         if (!D.scheme) CK(cudaMalloc(&D.scheme, sizeof(DevScheme)));
-        CK(cudaMemcpyAsync(D.words, p->host_words, size_t(p->n_words) * 4, cudaMemcpyHostToDevice, st));
-        if (n) {
-            CK(cudaMemcpyAsync(D.seq_pos, p->seq_pos.data(), size_t(n) * 8, cudaMemcpyHostToDevice, st));
-            CK(cudaMemcpyAsync(D.seq_len, p->seq_len.data(), size_t(n) * 8, cudaMemcpyHostToDevice, st));
+        if (!D.meta_ready) {
+            if (n) {
+                CK(cudaMemcpyAsync(D.seq_pos, p->seq_pos.data(), size_t(n) * 8, cudaMemcpyHostToDevice, st));
+                CK(cudaMemcpyAsync(D.seq_len, p->seq_len.data(), size_t(n) * 8, cudaMemcpyHostToDevice, st));
+            }
+            CK(cudaMemcpyAsync(D.scheme, &p->dev_scheme, sizeof(DevScheme), cudaMemcpyHostToDevice, st));
+            if (h2d) *h2d += n * 16 + int64_t(sizeof(DevScheme));
+            D.meta_ready = true;
         }
-        CK(cudaMemcpyAsync(D.scheme, &p->dev_scheme, sizeof(DevScheme), cudaMemcpyHostToDevice, st));
-        // the pinned words stream over PCIe while the host stages the tasks;
-        // batch creation waits for the stream before returning, so the image
-        // cannot be grown under an in-flight copy
-        if (h2d) *h2d += p->n_words * 4 + n * 16 + int64_t(sizeof(DevScheme));
-        D.ready = true;
+        D.resident.resize(size_t(n), 0);
+        // words still missing: one range per run of consecutive missing,
+        // needed sequences (merged across shared boundary words)
+        const int per = enc_per(p->enc);
+        std::vector<int64_t> ranges;  // (first word, words)
+        int64_t missing = 0;
+        if (need) {
+            for (int64_t i = 0; i < n; ++i) {
+                if (!(*need)[size_t(i)] || D.resident[size_t(i)]) continue;
+                const int64_t w0 = (p->seq_pos[size_t(i)]) / per;
+                const int64_t w1 = (p->seq_pos[size_t(i)] + std::max<int64_t>(p->seq_len[size_t(i)], 1) - 1) / per + 1;
+                if (!ranges.empty() && w0 <= ranges[ranges.size() - 2] + ranges.back()) {
+                    ranges.back() = std::max(ranges.back(), w1 - ranges[ranges.size() - 2]);
+                } else {
+                    ranges.push_back(w0);
+                    ranges.push_back(w1 - w0);
+                }
+            }
+            for (size_t r = 1; r < ranges.size(); r += 2) missing += ranges[r];
+        }
+        if (!need || 2 * missing > p->n_words) {
+            // the whole image (most of it is needed anyway: one contiguous copy)
+            CK(cudaMemcpyAsync(D.words, p->host_words, size_t(p->n_words) * 4, cudaMemcpyHostToDevice, st));
+            if (h2d) *h2d += p->n_words * 4;
+            D.ready = true;
+            D.resident.assign(size_t(n), 1);
+        } else if (missing) {
+            const int64_t nr = int64_t(ranges.size()) / 2;
+            if (nr <= 64) {  // few runs (a locality shard of a pool in genome order): copy them directly
+                for (int64_t r = 0; r < nr; ++r)
+                    CK(cudaMemcpyAsync(D.words + ranges[size_t(2 * r)], p->host_words + ranges[size_t(2 * r)],
+                                       size_t(ranges[size_t(2 * r + 1)]) * 4, cudaMemcpyHostToDevice, st));
+            } else {  // many runs: gather into one staged copy, scatter on the device
+                if (missing > D.cap_stage) {
+                    cudaFree(D.d_stage);
+                    CK(cudaMalloc(&D.d_stage, size_t(missing) * 4));
+                    D.cap_stage = missing;
+                }
+                if (nr > D.cap_ranges) {
+                    cudaFree(D.d_ranges);
+                    CK(cudaMalloc(&D.d_ranges, size_t(nr) * 24));
+                    D.cap_ranges = nr;
+                }
+                uint32_t* hs = nullptr;
+                int64_t* hr = nullptr;
+                CK(cudaMallocHost(&hs, size_t(missing) * 4));
+                CK(cudaMallocHost(&hr, size_t(nr) * 24));
+                int64_t at = 0;
+                for (int64_t r = 0; r < nr; ++r) {
+                    const int64_t w0 = ranges[size_t(2 * r)], len = ranges[size_t(2 * r + 1)];
+                    std::memcpy(hs + at, p->host_words + w0, size_t(len) * 4);
+                    hr[3 * r] = w0;
+                    hr[3 * r + 1] = at;
+                    hr[3 * r + 2] = len;
+                    at += len;
+                }
+                CK(cudaMemcpyAsync(D.d_stage, hs, size_t(missing) * 4, cudaMemcpyHostToDevice, st));
+                CK(cudaMemcpyAsync(D.d_ranges, hr, size_t(nr) * 24, cudaMemcpyHostToDevice, st));
+                scatter_words_kernel<<<unsigned(std::min<int64_t>(nr, 4096)), 256, 0, st>>>(D.d_stage, D.d_ranges,
+                                                                                        nr, D.words);
+                CK(cudaGetLastError());
+                CK(cudaStreamSynchronize(st));  // the staging buffers are released here
+                cudaFreeHost(hs);
+                cudaFreeHost(hr);
+            }
+            if (h2d) *h2d += missing * 4;
+            for (int64_t i = 0; i < n; ++i)
+                if ((*need)[size_t(i)]) D.resident[size_t(i)] = 1;
+        }
     }
     *out = &D;
     return XB_OK;
@@ -431,6 +522,8 @@ static void pool_drop_devices(xb_pool* p) {
         cudaFree(kv.second.seq_pos);
         cudaFree(kv.second.seq_len);
         cudaFree(kv.second.scheme);
+        cudaFree(kv.second.d_stage);
+        cudaFree(kv.second.d_ranges);
     }
     p->dev.clear();
 }
@@ -478,7 +571,8 @@ int64_t xb_pool_add_bulk(xb_pool* p, const char* concat, const int64_t* offsets,
     });
     if (bad) return -XB_E_UNKNOWN_SYMBOL;
     std::lock_guard<std::mutex> g(p->mu);
-    if (non_acgt && p->enc == ENC_2BIT && !widen_to_bytes(p)) return -XB_E_BAD_PARAM;
+    const bool widened = non_acgt && p->enc == ENC_2BIT;
+    if (widened && !widen_to_bytes(p)) return -XB_E_BAD_PARAM;
     const int64_t first = int64_t(p->offsets.size()) - 1;
     const int64_t at = p->offsets.back();
     const int64_t nw = words_for(p->enc, at + total);
@@ -508,7 +602,11 @@ int64_t xb_pool_add_bulk(xb_pool* p, const char* concat, const int64_t* offsets,
         p->seq_len.push_back(o1 - o0);
     }
     pool_scheme(p);
-    for (auto& kv : p->dev) kv.second.ready = false;
+    for (auto& kv : p->dev) {  // new sequences are not resident; a widened image none at all
+        kv.second.ready = false;
+        kv.second.meta_ready = false;
+        if (widened) kv.second.resident.clear();
+    }
     return first;
 }
 
@@ -528,7 +626,11 @@ int xb_pool_bits_per_symbol(const xb_pool* p) { return enc_bits(p->enc); }
 
 void xb_pool_evict(xb_pool* p) {
     std::lock_guard<std::mutex> g(p->mu);
-    for (auto& kv : p->dev) kv.second.ready = false;
+    for (auto& kv : p->dev) {
+        kv.second.ready = false;
+        kv.second.meta_ready = false;
+        kv.second.resident.clear();
+    }
 }
 
 void xb_pool_free(xb_pool* p) {
@@ -564,13 +666,20 @@ static CascadeOrder& cascade_order() {
 // copied to its start; the pilot's start tier is written by the kernel here.
 constexpr int kMiscStartTier = 1000;
 
+// Events of a run on its stream: start, after prep + sort, after the pilot,
+// after tier t (kEvTier + t), after the warp tier, after the result copy
+// (fetch), the cascade-order marker, and the early result copy.
+enum : int { kEvStart = 0, kEvPrep = 1, kEvPilot = 2, kEvTier = 3, kEvWarp = kEvTier + kWarpTier,
+             kEvFetch, kEvOrder, kEvCopy, kNumEv };
+static_assert(kNumEv <= 16, "Workspace::ev");
+
 struct Workspace {
     int dev = 0;
     bool in_use = false;
     int64_t capU = 0, capI = 0;
     size_t scratch_bytes = 0, cub_bytes = 0;
     cudaStream_t stream = nullptr;
-    cudaEvent_t ev[12] = {};
+    cudaEvent_t ev[16] = {};  // kEv* below
     int64_t* d_tasks = nullptr;
     DevUnit* d_units = nullptr;
     uint32_t *d_keys = nullptr, *d_vals = nullptr, *d_keys2 = nullptr, *d_order = nullptr;
@@ -579,7 +688,7 @@ struct Workspace {
     uint32_t* d_lists = nullptr;
     DevCounters* d_ctr = nullptr;
     int32_t* d_scratch = nullptr;
-    int32_t* d_resume = nullptr;  // kResumeCap escalation records
+    int32_t* d_resume = nullptr;  // narrow + wide escalation records (kResumeInts)
     int32_t* d_pilot = nullptr;
     void* d_cub = nullptr;
     DevResult* h_res = nullptr;
@@ -642,7 +751,7 @@ struct Workspace {
             CascadeOrder& o = cascade_order();
             std::lock_guard<std::mutex> g(o.mu);
             auto it = o.last.find(dev);
-            if (it != o.last.end() && it->second == ev[10]) o.last.erase(it);
+            if (it != o.last.end() && it->second == ev[kEvOrder]) o.last.erase(it);
         }
         cudaSetDevice(dev);
         release_units();
@@ -698,8 +807,8 @@ struct DevBatch {
     size_t cub_bytes = 0;
     cudaEvent_t* ev = nullptr;
     int sm_count = 0;
-    int occ[5] = {0, 0, 0, 0, 0};
-    int gocc[5] = {0, 0, 0, 0, 0};  // lane-group kernels
+    int occ[kWarpTier] = {};   // resident blocks per SM: thread kernels (0-4), wide kernels (5-8)
+    int gocc[kWarpTier] = {};  // lane-group kernels (0-4)
     int mode = 0;
     int launches = 0;
     // host staging (pinned)
@@ -735,7 +844,7 @@ constexpr size_t kIdleWorkspaces = 16;
 constexpr int64_t kIdleBytes = 8LL << 30;
 
 static int64_t ws_bytes(const Workspace* w) {
-    return w->capU * 160 + w->capI * 40 + int64_t(w->scratch_bytes) + int64_t(kResumeCap) * kResumeStride * 4;
+    return w->capU * 160 + w->capI * 40 + int64_t(w->scratch_bytes) + kResumeInts * 4;
 }
 
 static void free_dev(xb_pool*, DevBatch& D) {
@@ -781,7 +890,40 @@ static Workspace* acquire_workspace(int dev) {
     return w;
 }
 
-static int setup_device(xb_batch* B, DevBatch& D, const xb_exec* ex) {
+// The sequences a device's batch references (tasks: this device's shard;
+// units mode: its units), or an empty vector when the batch is dense enough
+// in references (every sequence in several tasks) that the whole pool is
+// needed anyway -- then the scan is skipped and the image goes up whole.
+static void referenced_sequences(const xb_batch* B, const DevBatch& D, const void* items,
+                                 std::vector<uint8_t>& need) {
+    const int64_t ns = int64_t(B->pool->seq_pos.size());
+    need.clear();
+    if (ns == 0 || 2 * D.n_items >= 8 * ns) return;
+    need.assign(size_t(ns), 0);
+    uint8_t* m = need.data();
+    const bool sh = !D.tasks.empty();
+    if (B->units_mode) {
+        const xb_unit* U = static_cast<const xb_unit*>(items);
+        parallel_for(D.n_items, [&](int64_t a, int64_t b) {
+            for (int64_t q = a; q < b; ++q) {
+                const xb_unit& u = U[sh ? D.tasks[size_t(q)] : q];
+                __atomic_store_n(&m[u.h_id], uint8_t(1), __ATOMIC_RELAXED);
+                __atomic_store_n(&m[u.v_id], uint8_t(1), __ATOMIC_RELAXED);
+            }
+        });
+    } else {
+        const xb_task* T = static_cast<const xb_task*>(items);
+        parallel_for(D.n_items, [&](int64_t a, int64_t b) {
+            for (int64_t q = a; q < b; ++q) {
+                const xb_task& t = T[sh ? D.tasks[size_t(q)] : q];
+                __atomic_store_n(&m[t.h_id], uint8_t(1), __ATOMIC_RELAXED);
+                __atomic_store_n(&m[t.v_id], uint8_t(1), __ATOMIC_RELAXED);
+            }
+        });
+    }
+}
+
+static int setup_device(xb_batch* B, DevBatch& D, const xb_exec* ex, const void* items) {
     CK(cudaSetDevice(D.dev));
     D.ws = acquire_workspace(D.dev);
     Workspace& W = *D.ws;
@@ -789,7 +931,7 @@ static int setup_device(xb_batch* B, DevBatch& D, const xb_exec* ex) {
         CK(cudaStreamCreateWithFlags(&W.stream, cudaStreamNonBlocking));
         for (auto& e : W.ev) CK(cudaEventCreate(&e));
         CK(cudaMalloc(&W.d_ctr, sizeof(DevCounters)));
-        CK(cudaMalloc(&W.d_resume, size_t(kResumeCap) * kResumeStride * 4));
+        CK(cudaMalloc(&W.d_resume, size_t(kResumeInts) * 4));
         CK(cudaStreamCreateWithFlags(&W.copy_stream, cudaStreamNonBlocking));
         int lo_pri = 0, hi_pri = 0;
         CK(cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri));
@@ -801,7 +943,9 @@ static int setup_device(xb_batch* B, DevBatch& D, const xb_exec* ex) {
     D.stream = (ex && ex->stream && B->devs.size() == 1) ? (cudaStream_t)ex->stream : W.stream;
     D.ev = W.ev;
     CK(cudaDeviceGetAttribute(&D.sm_count, cudaDevAttrMultiProcessorCount, D.dev));
-    const int rc = pool_device(B->pool, D.dev, D.stream, &B->h2d, &D.pool);
+    std::vector<uint8_t> need;
+    referenced_sequences(B, D, items, need);
+    const int rc = pool_device(B->pool, D.dev, D.stream, &B->h2d, &D.pool, need.empty() ? nullptr : &need);
     if (rc) return rc;
     const int64_t U = std::max<int64_t>(D.n_units, 1);
     if (U > W.capU) {
@@ -932,7 +1076,19 @@ static void* tier_fn_t(int t) {
     }
 }
 
+template <int MODE>
+static void* wide_fn_t(int t) {
+    switch (t) {
+        case 5: return reinterpret_cast<void*>(wide_tier_kernel<128, MODE>);
+        case 6: return reinterpret_cast<void*>(wide_tier_kernel<256, MODE>);
+        case 7: return reinterpret_cast<void*>(wide_tier_kernel<512, MODE>);
+        default: return reinterpret_cast<void*>(wide_tier_kernel<1024, MODE>);
+    }
+}
+
+// tiers 0-4: thread (or lane-group) kernels; 5-8: the wide one-warp-per-unit kernels
 static void* tier_kernel(bool group, int mode, int t) {
+    if (t >= kWideFirst) return mode == 0 ? wide_fn_t<0>(t) : mode == 1 ? wide_fn_t<1>(t) : wide_fn_t<2>(t);
     if (group) return mode == 0 ? tier_fn_t<true, 0>(t) : mode == 1 ? tier_fn_t<true, 1>(t) : tier_fn_t<true, 2>(t);
     return mode == 0 ? tier_fn_t<false, 0>(t) : mode == 1 ? tier_fn_t<false, 1>(t) : tier_fn_t<false, 2>(t);
 }
@@ -958,13 +1114,13 @@ static int run_plan(xb_batch* B, DevBatch& D) {
     const int mode = p->dev_scheme.fast_dna ? 0 : (p->enc == ENC_2BIT ? 1 : 2);
     const bool tok = thread_tiers_ok(p);
     D.launches = 0;
-    CK(cudaEventRecord(D.ev[0], D.stream));
+    CK(cudaEventRecord(D.ev[kEvStart], D.stream));
     CK(cudaMemsetAsync(D.d_ctr, 0, sizeof(DevCounters), D.stream));
     const int64_t nu = D.n_units;
     D.early_copy = false;
     D.t0 = -1;
     if (nu == 0) {
-        for (int q = 1; q < 9; ++q) CK(cudaEventRecord(D.ev[q], D.stream));
+        for (int q = kEvPrep; q <= kEvWarp; ++q) CK(cudaEventRecord(D.ev[q], D.stream));
         return XB_OK;
     }
     // ---- LR split + seed score + cost keys (or host-built units) ----
@@ -1013,6 +1169,9 @@ static int run_plan(xb_batch* B, DevBatch& D) {
         CK(cudaMemcpyAsync(&D.d_ctr->list_len[kWarpTier], &wlen, 8, cudaMemcpyHostToDevice, D.stream));
         CK(cudaStreamSynchronize(D.stream));  // host vectors die at scope end
     }
+    // units are ready: the pilot (below) may start on the aux stream while
+    // the main stream sorts them
+    CK(cudaEventRecord(D.aux_ev[0], D.stream));
     // ---- longest first ----
     const uint32_t* order = D.d_vals;
     if (!(B->flags & XB_FLAG_NO_SORT)) {
@@ -1021,7 +1180,7 @@ static int run_plan(xb_batch* B, DevBatch& D) {
                                                      D.d_order, int(nu), 0, 32, D.stream));
         order = D.d_order;
     }
-    CK(cudaEventRecord(D.ev[1], D.stream));
+    CK(cudaEventRecord(D.ev[kEvPrep], D.stream));
 
     TierParams tp{};
     tp.pool = D.pool->words;
@@ -1063,18 +1222,27 @@ static int run_plan(xb_batch* B, DevBatch& D) {
     tp.pilot_cap = 1024;
     tp.pilot_w = D.d_pilot;
     tp.esc_to_warp = (B->flags & XB_FLAG_ESC_TO_WARP) ? 1 : 0;
-    for (int t = 0; t < 5; ++t) {
+    for (int t = 0; t < kWarpTier; ++t) {
         if (!D.occ[t]) CK(occupancy_blocks(false, t, mode, &D.occ[t]) ? cudaErrorUnknown : cudaSuccess);
-        if (!D.gocc[t]) CK(occupancy_blocks(true, t, mode, &D.gocc[t]) ? cudaErrorUnknown : cudaSuccess);
+        if (t < kNarrowTiers && !D.gocc[t])
+            CK(occupancy_blocks(true, t, mode, &D.gocc[t]) ? cudaErrorUnknown : cudaSuccess);
     }
     if (pn > 0) {
-        tp.tier = 4;
-        tp.pilot = 1;
-        tp.role = kRoleAll;
+        // The pilot samples a stride of the units in input order (d_vals is
+        // the identity), so it needs only the prep kernel's units: it runs on
+        // the aux stream concurrently with the cost sort on the main stream.
+        TierParams pp = tp;
+        pp.order = D.d_vals;
+        pp.tier = 4;
+        pp.pilot = 1;
+        pp.role = kRoleAll;
         const bool g = !no_group;
         const long long lanes = pn * (g ? kGroupLanes : 1);
         const int blocks = int(std::min<long long>(D.sm_count * (g ? D.gocc[4] : D.occ[4]), (lanes + kTB - 1) / kTB));
-        CK(launch_tier(g, mode, 4, tp, blocks, D.stream));
+        CK(cudaStreamWaitEvent(D.aux_stream, D.aux_ev[0], 0));
+        CK(launch_tier(g, mode, 4, pp, blocks, D.aux_stream));
+        CK(cudaEventRecord(D.aux_ev[1], D.aux_stream));
+        CK(cudaStreamWaitEvent(D.stream, D.aux_ev[1], 0));
         ++D.launches;
     }
     tp.pilot = 0;
@@ -1082,7 +1250,7 @@ static int run_plan(xb_batch* B, DevBatch& D) {
                                                 D.h_misc + kMiscStartTier);
     CK(cudaGetLastError());
     ++D.launches;
-    CK(cudaEventRecord(D.ev[2], D.stream));
+    CK(cudaEventRecord(D.ev[kEvPilot], D.stream));
     D.tp = tp;
     D.all_group = all_group;
     D.no_group = no_group;
@@ -1098,9 +1266,7 @@ __global__ void gather_patch_kernel(TierParams P, int t0, uint32_t* __restrict__
         const uint32_t* L = P.lists + (long long)t * P.n_units;
         for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += stride) {
             const uint32_t e = L[i];
-            const uint32_t unit = (e & kResumeFlag)
-                                      ? uint32_t(P.resume[(long long)(e & ~kResumeFlag) * kResumeStride + kRecUnit])
-                                      : e;
+            const uint32_t unit = (e & kResumeFlag) ? uint32_t(record_ptr(P.resume, e)[kRecUnit]) : e;
             const unsigned long long slot = atomicAdd(&P.ctr->patch_n, 1ull);
             if ((long long)slot < cap) {
                 idx[slot] = unit;
@@ -1157,10 +1323,18 @@ static int run_cascade(xb_batch* B, DevBatch& D) {
         auto it = o.last.find(D.dev);
         if (it != o.last.end()) CK(cudaStreamWaitEvent(D.stream, it->second, 0));
     }
-    for (int t = 0; t < 5; ++t) {
+    for (int t = 0; t < kWarpTier; ++t) {
         tp.tier = t;
         if (t >= D.t0) {
-            if (D.all_group || D.no_group) {
+            if (t >= kWideFirst) {
+                // wide tiers (one warp per unit): the start tier's whole queue, or
+                // the escalations out of the K64 tier -- few units, so escalation
+                // launches get at most two blocks (8 warps) per SM
+                tp.role = t == D.t0 ? kRoleAll : kRoleEscalations;
+                const int per_sm = t == D.t0 ? D.occ[t] : std::min(D.occ[t], 2);
+                CK(launch_tier(false, mode, t, tp, D.sm_count * per_sm, D.stream));
+                ++D.launches;
+            } else if (D.all_group || D.no_group) {
                 tp.role = kRoleAll;
                 int per_sm = D.all_group ? D.gocc[t] : D.occ[t];
                 // latency mode: the escalation tiers after the start tier get no more
@@ -1171,18 +1345,10 @@ static int run_cascade(xb_batch* B, DevBatch& D) {
                 ++D.launches;
             } else if (t == D.t0) {  // the start tier: one thread per unit
                 if (concurrent) {
-                    // the next tier's list starts empty-marked; a few high-priority
-                    // lane-group blocks take its escalations while this tier runs
+                    // the next tier's list starts empty-marked
                     CK(cudaMemsetAsync(D.d_lists + int64_t(t + 1) * D.n_units, 0xFF, size_t(D.n_units) * 4,
                                        D.stream));
                     CK(cudaEventRecord(D.aux_ev[0], D.stream));
-                    CK(cudaStreamWaitEvent(D.aux_stream, D.aux_ev[0], 0));
-                    TierParams cp = tp;
-                    cp.tier = t + 1;
-                    cp.role = kRoleConsumer;
-                    CK(launch_tier(true, mode, t + 1, cp, kConsumerBlocks, D.aux_stream));
-                    CK(cudaEventRecord(D.aux_ev[1], D.aux_stream));
-                    ++D.launches;
                 }
                 tp.role = kRoleStart;
                 // leave the consumer's blocks room to be resident whichever kernel
@@ -1191,6 +1357,20 @@ static int run_cascade(xb_batch* B, DevBatch& D) {
                                std::max(1, D.sm_count * D.occ[t] - (concurrent ? kConsumerBlocks : 0)),
                                D.stream));
                 ++D.launches;
+                if (concurrent) {
+                    // a few high-priority lane-group blocks take the start tier's
+                    // escalations while it runs.  Launched after it (API order), so
+                    // tools that serialise launches run the consumer after the whole
+                    // start tier: the consumer never waits on a producer that cannot
+                    // run (no timeout, see group_tier_kernel)
+                    CK(cudaStreamWaitEvent(D.aux_stream, D.aux_ev[0], 0));
+                    TierParams cp = tp;
+                    cp.tier = t + 1;
+                    cp.role = kRoleConsumer;
+                    CK(launch_tier(true, mode, t + 1, cp, kConsumerBlocks, D.aux_stream));
+                    CK(cudaEventRecord(D.aux_ev[1], D.aux_stream));
+                    ++D.launches;
+                }
             } else {  // wider tiers: their escalations, on lane groups
                 tp.role = kRoleEscalations;
                 CK(launch_tier(true, mode, t, tp, D.sm_count * D.gocc[t], D.stream));
@@ -1198,15 +1378,15 @@ static int run_cascade(xb_batch* B, DevBatch& D) {
                 if (concurrent && t == D.t0 + 1) CK(cudaStreamWaitEvent(D.stream, D.aux_ev[1], 0));
             }
         }
-        CK(cudaEventRecord(D.ev[3 + t], D.stream));
+        CK(cudaEventRecord(D.ev[kEvTier + t], D.stream));
         if (t == D.t0 && D.capP > 0) {
-            CK(cudaStreamWaitEvent(D.copy_stream, D.ev[3 + t], 0));
+            CK(cudaStreamWaitEvent(D.copy_stream, D.ev[kEvTier + t], 0));
             CK(cudaMemcpyAsync(D.h_res, D.d_res, size_t(D.n_units) * sizeof(DevResult),
                                cudaMemcpyDeviceToHost, D.copy_stream));
             if (!B->units_mode && D.n_items)
                 CK(cudaMemcpyAsync(D.h_seed, D.d_seed, size_t(D.n_items) * 4, cudaMemcpyDeviceToHost,
                                    D.copy_stream));
-            CK(cudaEventRecord(D.ev[11], D.copy_stream));
+            CK(cudaEventRecord(D.ev[kEvCopy], D.copy_stream));
             D.early_copy = true;
             B->d2h += D.n_units * int64_t(sizeof(DevResult)) + (B->units_mode ? 0 : D.n_items * 4);
         }
@@ -1224,7 +1404,7 @@ static int run_cascade(xb_batch* B, DevBatch& D) {
         CK(cudaGetLastError());
         ++D.launches;
     }
-    CK(cudaEventRecord(D.ev[8], D.stream));
+    CK(cudaEventRecord(D.ev[kEvWarp], D.stream));
     if (D.early_copy) {
         gather_patch_kernel<<<unsigned(D.sm_count), 256, 0, D.stream>>>(tp, D.t0, D.d_patch_idx,
                                                                        D.d_patch_res, D.capP);
@@ -1232,8 +1412,8 @@ static int run_cascade(xb_batch* B, DevBatch& D) {
         ++D.launches;
     }
     if (order.owns_lock()) {
-        CK(cudaEventRecord(D.ev[10], D.stream));
-        cascade_order().last[D.dev] = D.ev[10];
+        CK(cudaEventRecord(D.ev[kEvOrder], D.stream));
+        cascade_order().last[D.dev] = D.ev[kEvOrder];
     }
     return XB_OK;
 }
@@ -1247,7 +1427,7 @@ static int fetch_device(xb_batch* B, DevBatch& D) {
     if (!B->units_mode && D.n_items)
         CK(cudaMemcpyAsync(D.h_seed, D.d_seed, size_t(D.n_items) * 4, cudaMemcpyDeviceToHost,
                            D.stream));
-    CK(cudaEventRecord(D.ev[9], D.stream));
+    CK(cudaEventRecord(D.ev[kEvFetch], D.stream));
     B->d2h += D.n_units * int64_t(sizeof(DevResult)) + (B->units_mode ? 0 : D.n_items * 4);
     return XB_OK;
 }
@@ -1268,6 +1448,92 @@ static void shard_lpt(const std::vector<long long>& cost, int G, std::vector<std
         out[size_t(e.second)].push_back(t);
         e.first += cost[size_t(t)];
         pq.push(e);
+    }
+    for (auto& v : out) std::sort(v.begin(), v.end());
+}
+
+// Estimated cost of each task: its two units' longest-first estimates (the
+// prep kernel's key), the linear proxy of SURVEY §8(e) for h_len * v_len
+// (partition.cpp:79-81).  The caller holds p->mu.
+static void task_costs(const xb_pool* p, const xb_task* tasks, int64_t n, int k, std::vector<long long>& cost) {
+    cost.resize(size_t(n));
+    parallel_for(n, [&](int64_t a, int64_t b) {
+        for (int64_t t = a; t < b; ++t) {
+            const xb_task& q = tasks[t];
+            const long long hl = p->offsets[q.h_id + 1] - p->offsets[q.h_id];
+            const long long vl = p->offsets[q.v_id + 1] - p->offsets[q.v_id];
+            cost[size_t(t)] = unit_est((long long)q.h_seed, (long long)q.v_seed) +
+                              unit_est(hl - (long long)q.h_seed - k, vl - (long long)q.v_seed - k) + 1;
+        }
+    });
+}
+
+// Locality-aware shards (the reference packs
+// sequences into IPU tiles with a greedy graph partition, partition.cpp:
+// 110-184).  Sequences are nodes, tasks edges.  Each
+// connected component is ordered by a breadth-first sweep started from a
+// peripheral node (the last node of a first BFS), so that neighbouring
+// sequences get nearby ranks -- on a read-overlap graph the sweep runs along
+// the genome.  Tasks are ordered by the lower rank of their two sequences
+// and cut into n_shards contiguous runs of equal estimated cost: each shard
+// references a compact neighbourhood of the pool, which is all a device
+// then uploads (pool_device's per-sequence residency).
+static void shard_locality(const xb_pool* p, const xb_task* tasks, int64_t n, const std::vector<long long>& cost,
+                           int G, std::vector<std::vector<int64_t>>& out) {
+    const int64_t ns = int64_t(p->offsets.size()) - 1;
+    std::vector<int64_t> deg(size_t(ns) + 1, 0);
+    for (int64_t t = 0; t < n; ++t) {
+        ++deg[tasks[t].h_id];
+        if (tasks[t].v_id != tasks[t].h_id) ++deg[tasks[t].v_id];
+    }
+    std::vector<int64_t> start(size_t(ns) + 1, 0);
+    for (int64_t i = 0; i < ns; ++i) start[size_t(i) + 1] = start[size_t(i)] + deg[size_t(i)];
+    std::vector<int64_t> adj(static_cast<size_t>(start[size_t(ns)]));
+    std::vector<int64_t> fill(start.begin(), start.end() - 1);
+    for (int64_t t = 0; t < n; ++t) {
+        const int64_t h = tasks[t].h_id, v = tasks[t].v_id;
+        adj[size_t(fill[size_t(h)]++)] = v;
+        if (v != h) adj[size_t(fill[size_t(v)]++)] = h;
+    }
+    std::vector<int64_t> rank(size_t(ns), -1), mark(size_t(ns), -1), queue;
+    queue.reserve(size_t(ns));
+    int64_t next_rank = 0;
+    auto bfs = [&](int64_t s, int64_t stamp, bool assign) {  // returns the last node reached
+        queue.clear();
+        queue.push_back(s);
+        mark[size_t(s)] = stamp;
+        for (size_t h = 0; h < queue.size(); ++h) {
+            const int64_t u = queue[h];
+            if (assign) rank[size_t(u)] = next_rank++;
+            for (int64_t e = start[size_t(u)]; e < start[size_t(u) + 1]; ++e) {
+                const int64_t w = adj[size_t(e)];
+                if (mark[size_t(w)] != stamp) {
+                    mark[size_t(w)] = stamp;
+                    queue.push_back(w);
+                }
+            }
+        }
+        return queue.back();
+    };
+    for (int64_t s = 0; s < ns; ++s) {
+        if (rank[size_t(s)] >= 0 || deg[size_t(s)] == 0) continue;
+        const int64_t far = bfs(s, 2 * s, false);
+        bfs(far, 2 * s + 1, true);
+    }
+    std::vector<int64_t> idx(static_cast<size_t>(n));
+    std::iota(idx.begin(), idx.end(), 0);
+    auto key = [&](int64_t t) { return std::min(rank[tasks[t].h_id], rank[tasks[t].v_id]); };
+    std::stable_sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) { return key(a) < key(b); });
+    long double total = 0;
+    for (long long c : cost) total += c;
+    out.assign(size_t(G), {});
+    long double acc = 0;
+    int g = 0;
+    for (int64_t t : idx) {
+        // cut where the running cost passes the next equal share
+        while (g < G - 1 && acc >= total * (g + 1) / G) ++g;
+        out[size_t(g)].push_back(t);
+        acc += cost[size_t(t)];
     }
     for (auto& v : out) std::sort(v.begin(), v.end());
 }
@@ -1365,16 +1631,13 @@ xb_batch* xb_batch_create(xb_pool* p, const xb_task* tasks, int64_t n, int k, in
     B->n = n;
     B->devs.resize(ids.size());
     if (ids.size() > 1) {
-        std::vector<long long> cost(static_cast<size_t>(n));
-        for (int64_t t = 0; t < n; ++t) {
-            const xb_task& q = tasks[t];
-            const long long hl = p->offsets[q.h_id + 1] - p->offsets[q.h_id];
-            const long long vl = p->offsets[q.v_id + 1] - p->offsets[q.v_id];
-            cost[size_t(t)] = unit_est(q.h_seed, q.v_seed) +
-                              unit_est(hl - q.h_seed - k, vl - q.v_seed - k) + 1;
-        }
+        std::vector<long long> cost;
+        task_costs(p, tasks, n, k, cost);
         std::vector<std::vector<int64_t>> sh;
-        shard_lpt(cost, int(ids.size()), sh);
+        if (B->flags & XB_FLAG_LOCALITY)
+            shard_locality(p, tasks, n, cost, int(ids.size()), sh);
+        else
+            shard_lpt(cost, int(ids.size()), sh);
         for (size_t g = 0; g < ids.size(); ++g) B->devs[g].tasks = std::move(sh[g]);
     }
     lk.unlock();
@@ -1383,7 +1646,7 @@ xb_batch* xb_batch_create(xb_pool* p, const xb_task* tasks, int64_t n, int k, in
         D.dev = ids[g];
         D.n_items = ids.size() > 1 ? int64_t(D.tasks.size()) : n;
         D.n_units = 2 * D.n_items;
-        rc = setup_device(B, D, exec);
+        rc = setup_device(B, D, exec, tasks);
         if (rc) return fail(rc, B);
         rc = upload_inputs(B, D, tasks);
         if (rc) return fail(rc, B);
@@ -1450,7 +1713,7 @@ int xb_batch_fetch(xb_batch* B, xb_side_result* out, int32_t* seed_score) {
             }
         };
         // bulk rows: on the host while the device may still be in the cascade tail
-        CK(cudaEventSynchronize(D.early_copy ? D.ev[11] : D.ev[9]));
+        CK(cudaEventSynchronize(D.early_copy ? D.ev[kEvCopy] : D.ev[kEvFetch]));
         copy_rows(D.h_res);
         if (seed_score && !B->units_mode) {
             if (!sharded)
@@ -1502,18 +1765,18 @@ int xb_batch_stats(xb_batch* B, xb_stats* st) {
         CK(cudaMemcpyAsync(D.h_misc, D.d_ctr, sizeof c, cudaMemcpyDeviceToHost, D.stream));
         CK(cudaStreamSynchronize(D.stream));
         std::memcpy(&c, D.h_misc, sizeof c);
-        float ms[10] = {0};
+        float ms[3 + kNumTiers] = {0};
         if (D.n_units) {
-            CK(cudaEventElapsedTime(&ms[0], D.ev[0], D.ev[8]));  // whole run
-            CK(cudaEventElapsedTime(&ms[1], D.ev[0], D.ev[1]));  // prep + sort
-            CK(cudaEventElapsedTime(&ms[2], D.ev[1], D.ev[2]));  // pilot + select
-            for (int t = 0; t < 5; ++t) CK(cudaEventElapsedTime(&ms[3 + t], D.ev[2 + t], D.ev[3 + t]));
-            CK(cudaEventElapsedTime(&ms[8], D.ev[7], D.ev[8]));  // warp tier
+            CK(cudaEventElapsedTime(&ms[0], D.ev[kEvStart], D.ev[kEvWarp]));  // whole run
+            CK(cudaEventElapsedTime(&ms[1], D.ev[kEvStart], D.ev[kEvPrep]));  // prep + sort
+            CK(cudaEventElapsedTime(&ms[2], D.ev[kEvPrep], D.ev[kEvPilot]));  // pilot + select
+            for (int t = 0; t < kNumTiers; ++t)  // tier t: from the previous tier's end (the pilot's for t = 0)
+                CK(cudaEventElapsedTime(&ms[3 + t], D.ev[kEvTier + t - 1], D.ev[kEvTier + t]));
         }
         st->ms_total = std::max(st->ms_total, double(ms[0]));
         st->ms_prep = std::max(st->ms_prep, double(ms[1]));
         st->ms_pilot = std::max(st->ms_pilot, double(ms[2]));
-        for (int t = 0; t < 6; ++t) {
+        for (int t = 0; t < kNumTiers; ++t) {
             st->ms_tier[t] = std::max(st->ms_tier[t], double(ms[3 + t]));
             st->units_tier[t] += int64_t(c.units[t]);
             st->cells_tier[t] += int64_t(c.cells[t]);
@@ -1621,7 +1884,7 @@ int xb_extend_units(xb_pool* p, const xb_unit* units, int64_t n, int band, xb_si
         }
         D.n_items = int64_t(D.h_units.size());
         D.n_units = D.n_items;
-        rc = setup_device(B, D, exec);
+        rc = setup_device(B, D, exec, units);
         if (!rc) rc = upload_inputs(B, D, nullptr);
         if (rc) {
             xb_batch_free(B);
@@ -1690,6 +1953,26 @@ int xb_sweep_band(uint64_t length, const int32_t* xs, int32_t nx, const double* 
     for (auto& t : th) t.join();
     for (int rc : rcs)
         if (rc) return rc;
+    return XB_OK;
+}
+
+int xb_shard_tasks(xb_pool* p, const xb_task* tasks, int64_t n, int k, int n_shards, int mode,
+                   int32_t* shard_of, int64_t* bad_task) {
+    if (!p || n < 0 || k < 0 || n_shards < 1 || (n && (!tasks || !shard_of)) ||
+        (mode != XB_SHARD_LPT && mode != XB_SHARD_LOCALITY))
+        return XB_E_BAD_PARAM;
+    std::lock_guard<std::mutex> g(p->mu);
+    const int rc = validate_tasks(p, tasks, n, k, bad_task);
+    if (rc) return rc;
+    std::vector<long long> cost;
+    task_costs(p, tasks, n, k, cost);
+    std::vector<std::vector<int64_t>> sh;
+    if (mode == XB_SHARD_LOCALITY)
+        shard_locality(p, tasks, n, cost, n_shards, sh);
+    else
+        shard_lpt(cost, n_shards, sh);
+    for (int s = 0; s < n_shards; ++s)
+        for (int64_t t : sh[size_t(s)]) shard_of[t] = s;
     return XB_OK;
 }
 

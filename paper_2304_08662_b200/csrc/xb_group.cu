@@ -41,11 +41,6 @@ __device__ __forceinline__ int gbfind64(uint64_t x) {
     asm("bfind.u64 %0, %1;" : "=r"(r) : "l"(x));
     return r;
 }
-__device__ __forceinline__ unsigned long long globaltimer_ns() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
 
 template <int LUT>
 __device__ __forceinline__ uint32_t glop3(uint32_t a, uint32_t b, uint32_t c) {
@@ -225,11 +220,12 @@ __device__ __forceinline__ void gfinish(GState<K, G, MODE>& S, const TierParams&
     if (code == kEscalate) {
         uint32_t entry = uint32_t(S.unit);
         if (sk.resumable) {
-            unsigned long long r = 0;
-            if (lane == 0) r = atomicAdd(&P.ctr->resume_next, 1ull);
-            r = __shfl_sync(gmask, r, 0, G);
-            if (r < (unsigned long long)kResumeCap) {
-                int32_t* rec = P.resume + (long long)r * kResumeStride;
+            int32_t* rec = nullptr;
+            uint32_t got = 0u;
+            if (lane == 0) got = alloc_record<K>(P, rec);
+            got = __shfl_sync(gmask, got, 0, G);
+            if (got) {
+                rec = record_ptr(P.resume, got);
 #pragma unroll
                 for (int s = 0; s < SS; ++s) {
                     rec[kRecRows + lane * SS + s] = cur[s];
@@ -250,7 +246,7 @@ __device__ __forceinline__ void gfinish(GState<K, G, MODE>& S, const TierParams&
                     rec[kRecLs2] = S.hs2 < 0 ? -1 : KB - S.lr2;
                     rec[kRecK] = K;
                 }
-                entry = kResumeFlag | uint32_t(r);
+                entry = got;
             }
         }
         if (lane == 0) {
@@ -560,6 +556,7 @@ __global__ void __launch_bounds__(128) group_tier_kernel(TierParams P) {
 
     Queue Q;
     if (!make_queue(P, Q)) return;
+    if (P.role != kRoleConsumer && Q.len == 0) return;  // nothing escalated into this tier
     if constexpr (MODE != 0) {
         tab_fill(tab, P.scheme, gap);
         __syncthreads();
@@ -597,12 +594,13 @@ __global__ void __launch_bounds__(128) group_tier_kernel(TierParams P) {
     // a claim it cannot serve and may stop at any time: the kRoleEscalations
     // launch after the start tier takes whatever is left), waits for the
     // claimed slot's entry to be written, and idles while nothing is queued.
+    // The handshake has no timeout: the start tier is launched (API order)
+    // before its consumer and never waits for it, so a consumer only ever
+    // waits on a producer that is running or already finished -- under tools
+    // that serialise launches (ncu, compute-sanitizer) it runs after the
+    // whole start tier and just drains the list.
     const bool consumer = P.role == kRoleConsumer;
     bool waiting = consumer;  // a consumer group with no unit, still looking for one
-    // Under serialising tools (ncu, compute-sanitizer) the start tier cannot
-    // run next to the consumer: if it has not started 5 ms after the consumer
-    // did, the consumer leaves everything to the kRoleEscalations launch.
-    const unsigned long long t_start = consumer ? globaltimer_ns() : 0ull;
     unsigned it = 0xFFFFFFFFu;
     auto fetch = [&]() __attribute__((always_inline)) {
         active = false;
@@ -617,10 +615,11 @@ __global__ void __launch_bounds__(128) group_tier_kernel(TierParams P) {
                     for (;;) {
                         const unsigned long long c = *curp;
                         if (c >= *lenp) {
-                            // the start tier (tier - 1) has taken no unit from its queue yet
-                            const bool alone = !*(volatile unsigned long long*)&P.ctr->cursor[P.tier - 1] &&
-                                               globaltimer_ns() - t_start > 5000000ull;
-                            st = (*(volatile int32_t*)&P.ctr->prod_finished || alone) ? 2 : 0;
+                            // nothing queued: done once the start tier has finished (the
+                            // list length is final then: its last block publishes the flag
+                            // after all of its escalations)
+                            st = *(volatile int32_t*)&P.ctr->prod_finished ? 2 : 0;
+                            if (st == 2 && c < *lenp) st = 0;  // a late entry landed meanwhile
                             break;
                         }
                         if (atomicCAS(Q.cursor, c, c + 1) == c) {
@@ -655,7 +654,7 @@ __global__ void __launch_bounds__(128) group_tier_kernel(TierParams P) {
             uint32_t unit = e;
             const int32_t* rec = nullptr;
             if (e & kResumeFlag) {
-                rec = P.resume + (long long)(e & ~kResumeFlag) * kResumeStride;
+                rec = record_ptr(P.resume, e);
                 unit = uint32_t(__ldcg(rec + kRecUnit));
             }
             const DevUnit u = P.units[unit];

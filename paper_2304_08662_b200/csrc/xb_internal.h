@@ -53,18 +53,20 @@ struct DevScheme {
     int32_t sim[32 * 32]; // code-pair scores [h][v] (sentinel row/col = very negative)
 };
 
-// Per-tier counters, device side (tiers: K16 K24 K32 K48 K64 warp).
+// Per-tier counters, device side (tiers: K16 K24 K32 K48 K64 | wide K128
+// K256 K512 K1024 | warp; cursor slot 15: the pilot).
 struct DevCounters {
-    unsigned long long cursor[8];      // work-queue cursors per tier (slot 7: pilot)
-    unsigned long long list_len[8];    // escalation-input list lengths per tier
-    unsigned long long units[8];
-    unsigned long long cells[8];
-    unsigned long long escalated[8];
+    unsigned long long cursor[16];     // work-queue cursors per tier (slot 15: pilot)
+    unsigned long long list_len[16];   // escalation-input list lengths per tier
+    unsigned long long units[16];
+    unsigned long long cells[16];
+    unsigned long long escalated[16];
     unsigned long long dbg[8];         // XB_COUNTERS builds: steps, rare, masked, recenters, stops;
                                        // [5] always: lane-group resumes at an even d
     int32_t start_tier;                // chosen by the pilot
     int32_t pad;
-    unsigned long long resume_next;    // resume records handed out
+    unsigned long long resume_next;    // narrow resume records handed out
+    unsigned long long resume_wide_next;  // wide resume records handed out
     unsigned long long patch_n;        // result rows finalised after the start tier
     unsigned int prod_done;            // start-tier blocks finished (concurrent escalation tail)
     int32_t prod_finished;             // 1 once every start-tier block has finished
@@ -74,14 +76,33 @@ struct DevCounters {
 // antidiagonal that did not fit, and the wider tier continues from there
 // instead of re-running it.  An escalation-list entry with kResumeFlag set
 // indexes a record; a plain entry is a unit to start from scratch (records
-// exhausted, or the next tier is the warp tier).
+// exhausted, or the next tier is the warp tier).  Writers with K <= 48 use
+// the narrow pool; K >= 64 writers (into the wide tiers) use the wide pool,
+// which follows the narrow one in the same buffer (kResumeWideFlag set).
 constexpr int kResumeCap = 32768;
 constexpr int kResumeStride = 128;  // int32 per record: 16 header + 2 * K_old row values
+constexpr int kResumeWideCap = 4096;
+constexpr int kResumeWideStride = 16 + 2 * 512;
+constexpr int64_t kResumeInts = int64_t(kResumeCap) * kResumeStride + int64_t(kResumeWideCap) * kResumeWideStride;
 constexpr uint32_t kResumeFlag = 0x80000000u;
+constexpr uint32_t kResumeWideFlag = 0x40000000u;
+constexpr uint32_t kResumeIndex = 0x3FFFFFFFu;
 enum : int {
     kRecUnit = 0, kRecD, kRecUbase, kRecTc, kRecBestD, kRecBestU, kRecCells, kRecDeltaW,
     kRecHs1, kRecLs1, kRecHs2, kRecLs2, kRecK, kRecRows = 16
 };
+
+#ifdef __CUDACC__
+#define XB_HD __host__ __device__
+#else
+#define XB_HD
+#endif
+// the record an escalation-list entry with kResumeFlag points at
+XB_HD inline int32_t* record_ptr(int32_t* resume, uint32_t e) {
+    const int64_t i = int64_t(e & kResumeIndex);
+    return (e & kResumeWideFlag) ? resume + int64_t(kResumeCap) * kResumeStride + i * kResumeWideStride
+                                 : resume + i * kResumeStride;
+}
 
 constexpr int kStatusOk = 0;
 constexpr int kStatusBand = 1;

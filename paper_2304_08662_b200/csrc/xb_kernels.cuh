@@ -65,12 +65,18 @@ __device__ __forceinline__ void tab_fill(tab_t* tab, const DevScheme* scheme, in
 constexpr int kTB = 128;                // threads per block, thread tiers
 constexpr int32_t kBig = 1 << 29;       // empty live range = [kBig, -kBig]
 
-// Thread tiers: band widths K (slots per unit); index 5 is the warp tier.
-constexpr int kNumTiers = 6;
-constexpr int kWarpTier = 5;
+// Tiers: band widths K (slots per unit).  0-4: thread / lane-group tiers
+// (K16..K64, register bands); 5-8: wide tiers (one warp per unit, K128..
+// K1024, xb_wide.cu); 9: the generic warp tier (any band).
+constexpr int kNumTiers = 10;
+constexpr int kNarrowTiers = 5;   // tiers 0..4
+constexpr int kWideFirst = 5;
+constexpr int kWarpTier = 9;
 __host__ __device__ constexpr int tier_width(int t) {
-    return t == 0 ? 16 : t == 1 ? 24 : t == 2 ? 32 : t == 3 ? 48 : t == 4 ? 64 : 1 << 30;
+    return t == 0 ? 16 : t == 1 ? 24 : t == 2 ? 32 : t == 3 ? 48 : t == 4 ? 64
+         : t == 5 ? 128 : t == 6 ? 256 : t == 7 ? 512 : t == 8 ? 1024 : 1 << 30;
 }
+constexpr int kPilotCursor = 15;  // DevCounters::cursor slot of the pilot sample
 
 struct TierParams {
     const uint32_t* __restrict__ pool;
@@ -90,7 +96,7 @@ struct TierParams {
     int32_t esc_to_warp;                 // escalations skip the wider thread tiers
     int32_t role;                        // kRole*: which of the tier's queues this launch serves
     int32_t* __restrict__ warp_scratch;  // warp tier: 2*band ints per warp slot
-    int32_t* __restrict__ resume;        // kResumeCap records of kResumeStride ints
+    int32_t* __restrict__ resume;        // narrow then wide resume records (xb_internal.h)
     // opaque constants: kept in c[]/uniform registers so ptxas cannot fold
     // them into ALU-pipe forms (LEA, LOP3 immediates, SEL)
     uint32_t pad0;                       // see the static_assert below
@@ -326,7 +332,7 @@ __device__ __forceinline__ bool make_queue(const TierParams& P, Queue& Q) {
         Q.q = P.order;
         Q.len = (unsigned long long)P.pilot_n;
         Q.stride = P.pilot_stride;
-        Q.cursor = &P.ctr->cursor[7];
+        Q.cursor = &P.ctr->cursor[kPilotCursor];
         return true;
     }
     const int t0 = P.ctr->start_tier;
@@ -345,6 +351,25 @@ __device__ __forceinline__ bool make_queue(const TierParams& P, Queue& Q) {
         Q.len = P.ctr->list_len[P.tier];
     }
     return true;
+}
+
+// Hands out a resume record for a K-slot writer: the escalation-list entry
+// (kResumeFlag, + kResumeWideFlag for the wide pool, | index) and the record,
+// or 0 when that pool is used up (the unit then restarts from scratch).
+template <int K>
+__device__ __forceinline__ uint32_t alloc_record(const TierParams& P, int32_t*& rec) {
+    static_assert(16 + 2 * K <= kResumeWideStride, "record too small for this writer");
+    if constexpr (16 + 2 * K <= kResumeStride) {
+        const unsigned long long r = atomicAdd(&P.ctr->resume_next, 1ull);
+        if (r >= (unsigned long long)kResumeCap) return 0u;
+        rec = P.resume + (long long)r * kResumeStride;
+        return kResumeFlag | uint32_t(r);
+    } else {
+        const unsigned long long r = atomicAdd(&P.ctr->resume_wide_next, 1ull);
+        if (r >= (unsigned long long)kResumeWideCap) return 0u;
+        rec = P.resume + (long long)kResumeCap * kResumeStride + (long long)r * kResumeWideStride;
+        return kResumeFlag | kResumeWideFlag | uint32_t(r);
+    }
 }
 
 // outcome of one antidiagonal step

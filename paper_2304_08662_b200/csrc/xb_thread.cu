@@ -336,9 +336,9 @@ __device__ __forceinline__ uint32_t save_resume(const TState<K, MODE>& S, const 
                                                 const int32_t (&prv)[K], const TierParams& P,
                                                 int32_t beta) {
     constexpr int KB = 32 * TState<K, MODE>::NM - 1;
-    const unsigned long long r = atomicAdd(&P.ctr->resume_next, 1ull);
-    if (r >= (unsigned long long)kResumeCap) return uint32_t(S.unit);
-    int32_t* rec = P.resume + (long long)r * kResumeStride;
+    int32_t* rec = nullptr;
+    const uint32_t entry = alloc_record<K>(P, rec);
+    if (!entry) return uint32_t(S.unit);
     rec[kRecUnit] = S.unit;
     rec[kRecD] = S.d;
     rec[kRecUbase] = S.ubase;
@@ -357,7 +357,7 @@ __device__ __forceinline__ uint32_t save_resume(const TState<K, MODE>& S, const 
         rec[kRecRows + k] = cur[k];
         rec[kRecRows + K + k] = prv[k];
     }
-    return kResumeFlag | uint32_t(r);
+    return entry;
 }
 
 // Records the outcome of the current unit at the step that decides it (the
@@ -627,7 +627,7 @@ __global__ void __launch_bounds__(kTB, tier_min_blocks<K, MODE>()) thread_tier_k
             uint32_t unit = e;
             const int32_t* rec = nullptr;
             if (e & kResumeFlag) {
-                rec = P.resume + (long long)(e & ~kResumeFlag) * kResumeStride;
+                rec = record_ptr(P.resume, e);
                 unit = uint32_t(rec[kRecUnit]);
             }
             // units whose values could leave the drift-space range go to the warp tier
@@ -705,7 +705,7 @@ XB_INST(64)
 // choice also goes straight to pinned host memory (host_out), so the host's
 // read-back does not queue behind other batches' copies on a copy engine.
 __global__ void select_tier_kernel(TierParams P, int forced, int32_t* host_out) {
-    __shared__ unsigned long long need[6];  // sample units needing more than tier t
+    __shared__ unsigned long long need[kNarrowTiers];  // sample units needing more than tier t
     __shared__ unsigned long long nn;
     if (blockIdx.x != 0) return;
     if (forced >= 0) {
@@ -715,18 +715,18 @@ __global__ void select_tier_kernel(TierParams P, int forced, int32_t* host_out) 
         }
         return;
     }
-    if (threadIdx.x < 6) need[threadIdx.x] = 0;
+    if (threadIdx.x < kNarrowTiers) need[threadIdx.x] = 0;
     if (threadIdx.x == 0) nn = 0;
     __syncthreads();
-    unsigned long long my_need[5] = {0, 0, 0, 0, 0}, my_n = 0;
+    unsigned long long my_need[kNarrowTiers] = {0, 0, 0, 0, 0}, my_n = 0;
     for (long long q = threadIdx.x; q < P.pilot_n; q += blockDim.x) {
         const int pw = P.pilot_w[q];
         if (pw == -2) continue;
         const int w = pw < 0 ? (1 << 30) : pw + 2;  // +2: unclamped-window slack
         ++my_n;
-        for (int t = 0; t < 5; ++t) my_need[t] += w > tier_width(t) && P.band > tier_width(t);
+        for (int t = 0; t < kNarrowTiers; ++t) my_need[t] += w > tier_width(t) && P.band > tier_width(t);
     }
-    for (int t = 0; t < 5; ++t)
+    for (int t = 0; t < kNarrowTiers; ++t)
         if (my_need[t]) atomicAdd(&need[t], my_need[t]);
     if (my_n) atomicAdd(&nn, my_n);
     __syncthreads();
@@ -734,14 +734,17 @@ __global__ void select_tier_kernel(TierParams P, int forced, int32_t* host_out) 
     const double n = double(nn);
     int best = 4;
     double best_cost = 1e30;
-    for (int t = 0; t < 5; ++t) {
+    for (int t = 0; t < kNarrowTiers; ++t) {
         double cost = tier_width(t);
-        for (int u = t + 1; u < 5; ++u) cost += 1.5 * tier_width(u) * (n > 0 ? double(need[u - 1]) / n : 0.0);
+        for (int u = t + 1; u < kNarrowTiers; ++u)
+            cost += 1.5 * tier_width(u) * (n > 0 ? double(need[u - 1]) / n : 0.0);
         if (cost < best_cost) {
             best_cost = cost;
             best = t;
         }
     }
+    // most of the sample outgrows K64: the whole batch starts on the wide tiers
+    if (n > 0 && double(need[kNarrowTiers - 1]) > 0.5 * n) best = kWideFirst;
     P.ctr->start_tier = best;
     *(volatile int32_t*)host_out = best;
 }

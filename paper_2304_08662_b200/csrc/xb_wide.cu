@@ -1,0 +1,620 @@
+// Wide tiers: one warp per unit, K = 128 / 256 / 512 / 1024 slots of the
+// restricted band in registers (S = K/32 consecutive slots per lane).  They
+// take the units whose live window outgrows the K64 tier -- large X, low
+// identity, the reference's default band of 1024 (pipeline.hpp:28) -- which
+// round 1 left to the generic warp tier's global-memory rows.
+//
+// Exact reference semantics (proj/src/align.cpp:37-155), same coordinates,
+// drift-space values and window bookkeeping as the thread tier (see
+// xb_kernels.cuh and xb_thread.cu).  What differs from the narrow tiers:
+//   * the running best is carried in plain drift-space values, not 64x keys
+//     (a slot index no longer fits 6 bits): the drop test of slot k is
+//     s_k < max(Tv, max over earlier cells of s_j - X), a lane-local chain
+//     seeded by a warp suffix-max over the higher lanes (5 shuffle rounds);
+//   * the first cell attaining a new best (the reference's strict '>' in
+//     ascending i) is the highest lane holding the antidiagonal maximum, and
+//     within it the highest slot: one ballot, taken only on antidiagonals
+//     that raise T (warp-uniform: the warp holds one unit);
+//   * the live range is two warp reductions (max of the highest live slot,
+//     min of the lowest) instead of a gathered bit mask;
+//   * a recentre shifts the rows through shared memory (rare).
+// Control flow is warp-uniform throughout: one unit per warp.
+#include <climits>
+#include <cstdint>
+
+#include "xb_kernels.cuh"
+
+namespace xb {
+
+namespace {
+
+__device__ __forceinline__ uint32_t wbits(int lo, int hi) {
+    if (lo > hi) return 0u;
+    return (0xFFFFFFFFu >> (31 - hi)) & (0xFFFFFFFFu << lo);
+}
+
+__device__ __forceinline__ int wbfind(uint32_t x) {
+    int r;
+    asm("bfind.u32 %0, %1;" : "=r"(r) : "r"(x));
+    return r;
+}
+
+template <int LUT>
+__device__ __forceinline__ uint32_t wlop3(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(d) : "r"(a), "r"(b), "r"(c), "n"(LUT));
+    return d;
+}
+
+constexpr int kWideWarps = 4;  // warps (units) per block
+
+}  // namespace
+
+template <int K, int MODE>
+struct WState {
+    static constexpr int S = K / 32;           // slots per lane
+    static constexpr int NW = (S + 15) / 16;   // 2-bit window words per lane (MODE 0)
+    static constexpr int NB = (S + 3) / 4;     // byte window words per lane (table modes)
+    static constexpr int KB = K - 1;
+    int64_t h_pos, v_pos;
+    int32_t m, n, hdir, vdir, unit;
+    int32_t d, ubase;
+    int32_t lr1, hs1, lr2, hs2;  // hs / KB - ls of rows d-1, d-2; -1 for an empty row
+    int32_t d_vm, d_lim, stop;
+    int32_t Tv;                  // T + beta d + 1: the chain's start (= Tc / 64 of the narrow tiers)
+    int32_t best_d, best_u, cells, delta_w;
+    uint32_t VW[NW], HW[NW];     // 2-bit windows of this lane's S slots (MODE 0)
+    uint32_t VWb[NB], HWb[NB];   // byte windows (table modes)
+    static constexpr int RENC = MODE == 2 ? ENC_8BIT : ENC_2BIT;
+    static constexpr int RPER = EncFields<RENC>::PER;
+    Reader<true, RENC> rv;       // lane 0: v symbols entering slot 0
+    Reader<false, RENC> rh;      // lane 31: h symbols entering slot K-1
+};
+
+template <int K, int MODE>
+__device__ __forceinline__ void w_limits(WState<K, MODE>& S) {
+    S.d_vm = min(2 * (S.ubase + S.n + 1), 2 * (S.m - S.ubase - K + 2) - 1);
+    S.d_lim = min(S.d_vm, S.n + S.m + 2);
+}
+
+// symbol windows of this lane's slots at antidiagonal S.d, readers set up for
+// rv_r / rh_r symbols before their next refill point (lanes 0 / 31)
+template <int K, int MODE>
+__device__ __forceinline__ void w_windows(WState<K, MODE>& S, const uint32_t* __restrict__ pool, int lane,
+                                          int rv_r, int rh_r) {
+    using St = WState<K, MODE>;
+    constexpr int SS = St::S;
+    const int fd = S.d >> 1, cd = S.d - fd;
+    const int64_t a = int64_t(fd) - S.ubase - 1;  // v index of global slot 0
+    const int64_t b = int64_t(cd) + S.ubase - 1;  // h index of global slot 0
+    const int k0 = lane * SS;
+    if constexpr (MODE == 0) {
+#pragma unroll
+        for (int w = 0; w < St::NW; ++w) {
+            const int n_in = min(16, SS - 16 * w);
+            const uint32_t keep = n_in >= 16 ? 0xFFFFFFFFu : ((1u << (2 * n_in)) - 1u);
+            // slot s of word w <- v[a - k0 - 16w - s] at bits 2s; h[b + k0 + 16w + s]
+            S.VW[w] = chunk_tf(pool, S.v_pos, S.vdir, a - k0 - 16 * w - 15);  // slots >= n_in: unused
+            S.HW[w] = chunk_bf(pool, S.h_pos, S.hdir, b + k0 + 16 * w) & keep;
+        }
+    } else {
+        constexpr int ENC = MODE == 1 ? ENC_2BIT : ENC_8BIT;
+#pragma unroll
+        for (int r = 0; r < St::NB; ++r) {
+            uint32_t vw = 0, hw = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int s = 4 * r + q;
+                if (s < SS) {
+                    vw |= code_at<ENC>(pool, S.v_pos, S.vdir, S.n, a - k0 - s) << (8 * q);
+                    hw |= code_at<ENC>(pool, S.h_pos, S.hdir, S.m, b + k0 + s) << (8 * q);
+                }
+            }
+            S.VWb[r] = vw;
+            S.HWb[r] = hw;
+        }
+    }
+    if (lane == 0) S.rv.init(pool, S.v_pos, S.vdir, a + 1, rv_r);
+    if (lane == 31) S.rh.init(pool, S.h_pos, S.hdir, b + K, rh_r);
+}
+
+// Table modes: sentinel bytes over slots whose v or h symbol lies past the
+// view's end (see the thread tier's sentinel_windows).
+template <int K, int MODE>
+__device__ __forceinline__ void w_sentinels(WState<K, MODE>& S, int d, int k0) {
+    using St = WState<K, MODE>;
+    const int fd = d >> 1, cd = d - fd;
+    const int vhi = fd - S.ubase - 1 - S.n - k0;
+    const int hlo = S.m - (cd + S.ubase - 1) - k0;
+#pragma unroll
+    for (int r = 0; r < St::NB; ++r) {
+        const int v1 = min(vhi - 4 * r, 3), h0 = max(hlo - 4 * r, 0);
+        const uint32_t mv = v1 < 0 ? 0u : wbits(0, 8 * v1 + 7);
+        const uint32_t mh = h0 > 3 ? 0u : wbits(8 * h0, 31);
+        S.VWb[r] = (S.VWb[r] & ~mv) | (0x1F1F1F1Fu & mv);
+        S.HWb[r] = (S.HWb[r] & ~mh) | (0x1F1F1F1Fu & mh);
+    }
+}
+
+// rows shifted by sh slots across the warp (new slot k = old slot k + sh,
+// vacated slots dead) through this warp's shared-memory row
+template <int SS>
+__device__ __forceinline__ void w_shift(int32_t (&R)[SS], int sh, int lane, int32_t* row) {
+    constexpr int KK = 32 * SS;
+    __syncwarp();
+#pragma unroll
+    for (int s = 0; s < SS; ++s) row[lane * SS + s] = R[s];
+    __syncwarp();
+#pragma unroll
+    for (int s = 0; s < SS; ++s) {
+        const int src = lane * SS + s + sh;
+        R[s] = (src >= 0 && src < KK) ? row[src] : kDeadS;
+    }
+    __syncwarp();
+}
+
+template <int K, int MODE, bool ODD>
+__device__ __forceinline__ void wfeed(WState<K, MODE>& S, int lane) {
+    using St = WState<K, MODE>;
+    constexpr int SS = St::S;
+    if constexpr (MODE == 0) {
+        constexpr int NW = St::NW;
+        constexpr int top = 2 * ((SS - 1) & 15);  // bit offset of slot SS-1 in the last word
+        if constexpr (ODD) {  // v: slot k <- k-1, new symbol at slot 0 (lane 0's reader)
+            const uint32_t out = (S.VW[NW - 1] >> top) & 3u;
+            uint32_t in = __shfl_up_sync(0xFFFFFFFFu, out, 1);
+            if (lane == 0) {
+                in = S.rv.cur >> 30;
+                S.rv.cur <<= 2;
+            }
+#pragma unroll
+            for (int w = NW - 1; w > 0; --w) S.VW[w] = __funnelshift_l(S.VW[w - 1], S.VW[w], 2);
+            S.VW[0] = (S.VW[0] << 2) | in;
+        } else {  // h: slot k <- k+1, new symbol at slot K-1 (lane 31's reader)
+            const uint32_t out = S.HW[0] & 3u;
+            uint32_t in = __shfl_down_sync(0xFFFFFFFFu, out, 1);
+            if (lane == 31) {
+                in = S.rh.cur & 3u;
+                S.rh.cur >>= 2;
+            }
+#pragma unroll
+            for (int w = 0; w < NW - 1; ++w) S.HW[w] = __funnelshift_r(S.HW[w], S.HW[w + 1], 2);
+            const uint32_t keep = top == 30 ? 0xFFFFFFFFu : ((1u << (top + 2)) - 1u);
+            S.HW[NW - 1] = ((S.HW[NW - 1] >> 2) & (keep >> 2)) | (in << top);
+        }
+    } else {
+        constexpr int NB = St::NB;
+        constexpr int top = 8 * ((SS - 1) & 3);
+        if constexpr (ODD) {
+            const uint32_t out = (S.VWb[NB - 1] >> top) & 0xFFu;
+            uint32_t in = __shfl_up_sync(0xFFFFFFFFu, out, 1);
+            if (lane == 0) in = S.rv.take();
+#pragma unroll
+            for (int r = NB - 1; r > 0; --r) S.VWb[r] = __funnelshift_l(S.VWb[r - 1], S.VWb[r], 8);
+            S.VWb[0] = (S.VWb[0] << 8) | in;
+        } else {
+            const uint32_t out = S.HWb[0] & 0xFFu;
+            uint32_t in = __shfl_down_sync(0xFFFFFFFFu, out, 1);
+            if (lane == 31) in = S.rh.take();
+#pragma unroll
+            for (int r = 0; r < NB - 1; ++r) S.HWb[r] = __funnelshift_r(S.HWb[r], S.HWb[r + 1], 8);
+            const uint32_t keep = top == 24 ? 0xFFFFFFFFu : ((1u << (top + 8)) - 1u);
+            S.HWb[NB - 1] = ((S.HWb[NB - 1] >> 8) & (keep >> 8)) | (in << top);
+        }
+    }
+}
+
+struct WSink {
+    uint32_t* esc_list;
+    unsigned long long* esc_len;
+    unsigned long long units, cells, esc;
+    bool resumable;
+};
+
+// Records the outcome of the warp's unit at the deciding step (see the
+// thread tier's finish_unit).
+template <int K, int MODE>
+__device__ __forceinline__ void wfinish(WState<K, MODE>& S, const TierParams& P, int code, int spread,
+                                        WSink& sk, int32_t beta, const int32_t (&cur)[K / 32],
+                                        const int32_t (&prv)[K / 32], int lane) {
+    constexpr int SS = K / 32;
+    constexpr int KB = WState<K, MODE>::KB;
+    S.stop = code;
+    if (code == kEscalate) {
+        uint32_t entry = uint32_t(S.unit);
+        if constexpr (K < tier_width(kWarpTier - 1))  // the widest tier hands bare units to the warp tier
+        if (sk.resumable) {
+            int32_t* rec = nullptr;
+            uint32_t got = 0u;
+            if (lane == 0) got = alloc_record<K>(P, rec);
+            got = __shfl_sync(0xFFFFFFFFu, got, 0);
+            if (got) {
+                rec = record_ptr(P.resume, got);
+#pragma unroll
+                for (int s = 0; s < SS; ++s) {
+                    rec[kRecRows + lane * SS + s] = cur[s];
+                    rec[kRecRows + K + lane * SS + s] = prv[s];
+                }
+                if (lane == 0) {
+                    rec[kRecUnit] = S.unit;
+                    rec[kRecD] = S.d;
+                    rec[kRecUbase] = S.ubase;
+                    rec[kRecTc] = (S.Tv - beta) << 6;  // as before step d, in 64x chain units
+                    rec[kRecBestD] = S.best_d;
+                    rec[kRecBestU] = S.best_u;
+                    rec[kRecCells] = S.cells;
+                    rec[kRecDeltaW] = S.delta_w;
+                    rec[kRecHs1] = S.hs1;
+                    rec[kRecLs1] = S.hs1 < 0 ? -1 : KB - S.lr1;
+                    rec[kRecHs2] = S.hs2;
+                    rec[kRecLs2] = S.hs2 < 0 ? -1 : KB - S.lr2;
+                    rec[kRecK] = K;
+                }
+                entry = got;
+            }
+        }
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence();
+            const unsigned long long slot = atomicAdd(sk.esc_len, 1ull);
+            sk.esc_list[slot] = entry;
+            ++sk.esc;
+        }
+        return;
+    }
+    if (lane != 0) return;
+    DevResult res;
+    res.cells = S.cells;
+    res.delta_w = S.delta_w;
+    if (code == kBand) {
+        res.score = res.h_ext = res.v_ext = 0;
+        res.status = kStatusBand;
+        res.spread = spread;
+    } else {
+        const int best_i = (S.best_d >> 1) - S.best_u;
+        res.score = S.Tv - beta * S.d - 1;
+        res.h_ext = S.best_d - best_i;
+        res.v_ext = best_i;
+        res.status = kStatusOk;
+        res.spread = 0;
+    }
+    P.results[S.unit] = res;
+    ++sk.units;
+    sk.cells += (unsigned long long)S.cells;
+}
+
+// One antidiagonal d.  cur holds d-2 on entry and d on exit, prv holds d-1.
+template <int K, int MODE, bool ODD>
+__device__ __forceinline__ void wstep(WState<K, MODE>& S, int32_t (&cur)[K / 32], int32_t (&prv)[K / 32],
+                                      const TierParams& P, const tab_t* __restrict__ tab, int32_t gap,
+                                      int32_t X, unsigned it, int lane, WSink& sk, int32_t* srow) {
+    using St = WState<K, MODE>;
+    constexpr int SS = St::S;
+    constexpr int KB = St::KB;
+    const int d = S.d;
+    const int k0 = lane * SS;
+    const int32_t beta = -gap;
+    S.Tv += beta;
+    // window of row d, unclamped below d_vm (see the thread tier's xstep)
+    const int M = ODD ? max(S.lr1 + 1, S.lr2) : max(S.lr1, S.lr2);  // KB - s_lo
+    const int s_hi = ODD ? max(S.hs1, S.hs2) : max(S.hs1 + 1, S.hs2);
+    int wm1 = s_hi + M - KB;
+    uint32_t vml = wbits(0, SS - 1);  // this lane's in-matrix slots
+    [[maybe_unused]] uint32_t inv[St::NW];
+#pragma unroll
+    for (int w = 0; w < St::NW; ++w) inv[w] = 0u;
+    // warp-uniform rare path
+    if (M > KB || unsigned(s_hi) > unsigned(K - 1) || unsigned(wm1) >= unsigned(P.band) || d >= S.d_lim) {
+        const bool e1 = S.hs1 < 0, e2 = S.hs2 < 0;
+        if ((e1 && e2) || d > S.n + S.m + 1) {
+            wfinish<K, MODE>(S, P, kDone, 0, sk, beta, cur, prv, lane);
+            return;
+        }
+        int lo = kBig, hi = -kBig;
+        if (!e1) {
+            lo = KB - S.lr1 - (ODD ? 1 : 0);
+            hi = S.hs1 + (ODD ? 0 : 1);
+        }
+        if (!e2) {
+            lo = min(lo, KB - S.lr2);
+            hi = max(hi, S.hs2);
+        }
+        const int fd = d >> 1;
+        int A = fd - S.ubase;
+        const int w = min(hi, A - max(d - S.m, 0)) - max(lo, A - min(d, S.n)) + 1;
+        if (w > P.band) {
+            wfinish<K, MODE>(S, P, kBand, w, sk, beta, cur, prv, lane);
+            return;
+        }
+        if (lo < 0 || hi > K - 1) {
+            const int wu = hi - lo + 1;
+            if (wu > K) {
+                wfinish<K, MODE>(S, P, kEscalate, 0, sk, beta, cur, prv, lane);
+                return;
+            }
+            const int sh = lo - ((K - wu) >> 1);  // new slot 0 = old slot sh
+            w_shift<SS>(cur, sh, lane, srow);
+            w_shift<SS>(prv, sh, lane, srow);
+            S.ubase += sh;
+            if (!e1) {
+                S.hs1 -= sh;
+                S.lr1 += sh;
+            }
+            if (!e2) {
+                S.hs2 -= sh;
+                S.lr2 += sh;
+            }
+            A -= sh;
+            w_limits(S);
+            constexpr int PER = St::RPER;
+            const int to_refill = PER - int(it & (PER - 1));
+            w_windows(S, P.pool, lane, ODD ? to_refill : to_refill - 1, to_refill);
+        }
+        if (d >= S.d_vm) {
+            // slots inside the matrix: i <= n  <=>  k >= klo ;  j <= m  <=>  k <= khi
+            const int klo = A - S.n;
+            const int khi = S.m - (d - fd) - S.ubase;
+            const int l = max(klo - k0, 0), h = min(min(khi, K - 1) - k0, SS - 1);
+            vml = wbits(l, h);
+            if constexpr (MODE == 0) {
+#pragma unroll
+                for (int ww = 0; ww < St::NW; ++ww) {
+                    const int lw = max(l - 16 * ww, 0), hw = min(h - 16 * ww, 15);
+                    inv[ww] = ~((lw > hw) ? 0u : wbits(2 * lw, 2 * hw + 1));
+                }
+            } else {
+                w_sentinels(S, d, k0);
+            }
+        }
+        wm1 = max(w, 0) - 1;  // a clamped-empty row counts no cells (align.cpp:84-90)
+    }
+    S.cells += wm1 + 1;
+    S.delta_w = max(S.delta_w, wm1 + 1);
+
+    // gap source across the lane edge
+    int32_t edge;
+    if constexpr (ODD) {
+        edge = __shfl_down_sync(0xFFFFFFFFu, prv[0], 1);
+        if (lane == 31) edge = kDeadS;
+    } else {
+        edge = __shfl_up_sync(0xFFFFFFFFu, prv[SS - 1], 1);
+        if (lane == 0) edge = kDeadS;
+    }
+    // match bytes (see the thread tier): byte j of Z[w][q] = 1 + 2*match of slot 16w + 4j + q
+    [[maybe_unused]] uint32_t Z[St::NW][4];
+    if constexpr (MODE == 0) {
+#pragma unroll
+        for (int ww = 0; ww < St::NW; ++ww) {
+            const uint32_t x = wlop3<0xBE>(S.VW[ww], S.HW[ww], inv[ww]);  // (a ^ b) | c
+            const uint32_t z = ~(x | (x << 1));
+#pragma unroll
+            for (int q = 0; q < 4; ++q) Z[ww][q] = ((z >> (2 * q)) & 0x02020202u) | 0x01010101u;
+        }
+    }
+    // pass 1: candidates; lane maximum and its highest slot (key = 64 cand + s)
+    int32_t cand[SS];
+    int32_t mk = -(1 << 30);
+#pragma unroll
+    for (int s = SS - 1; s >= 0; --s) {
+        const int32_t dg = cur[s];
+        int32_t db;
+        if constexpr (MODE == 0) {
+            db = __dp4a(int(Z[s >> 4][s & 3]), 1 << (8 * ((s >> 2) & 3)), dg);
+        } else {
+            const int r = s >> 2, q = s & 3;
+            uint32_t idx = 0;
+            switch (q) {  // bytes: v code, h code, 0, 0
+                case 0: asm("prmt.b32 %0, %1, %2, 0x8840;" : "=r"(idx) : "r"(S.VWb[r]), "r"(S.HWb[r])); break;
+                case 1: asm("prmt.b32 %0, %1, %2, 0x9951;" : "=r"(idx) : "r"(S.VWb[r]), "r"(S.HWb[r])); break;
+                case 2: asm("prmt.b32 %0, %1, %2, 0xAA62;" : "=r"(idx) : "r"(S.VWb[r]), "r"(S.HWb[r])); break;
+                default: asm("prmt.b32 %0, %1, %2, 0xBB73;" : "=r"(idx) : "r"(S.VWb[r]), "r"(S.HWb[r])); break;
+            }
+            db = dg + tab_lookup(tab, idx);
+        }
+        int32_t ln, un;
+        if constexpr (ODD) {  // gap sources at u and u+1
+            ln = prv[s];
+            un = s < SS - 1 ? prv[s < SS - 1 ? s + 1 : s] : edge;
+        } else {              // gap sources at u-1 and u
+            ln = s > 0 ? prv[s > 0 ? s - 1 : s] : edge;
+            un = prv[s];
+        }
+        cand[s] = __vimax3_s32(db, ln, un);
+        mk = max(mk, cand[s] * 64 + s);
+    }
+    const int32_t mv = mk >> 6;  // lane maximum (drift space)
+    // suffix maximum over the lanes (ascending i = descending lane)
+    int32_t incl = mv;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_down_sync(0xFFFFFFFFu, incl, o);
+        if (lane + o < 32) incl = max(incl, y);
+    }
+    int32_t above = __shfl_down_sync(0xFFFFFFFFu, incl, 1);
+    if (lane == 31) above = -(1 << 30);
+    const int32_t gmax = __shfl_sync(0xFFFFFFFFu, incl, 0);
+    // pass 2: the lane's chain (align.cpp:122-129: prune against the running
+    // best, which includes the cell itself), drop test, live bits
+    int32_t c = max(S.Tv, above - X);
+    uint32_t dm = 0u;
+#pragma unroll
+    for (int s = SS - 1; s >= 0; --s) {
+        c = __viaddmax_s32(cand[s], -X, c);
+        if (cand[s] < c) {
+            cand[s] = kDeadS;
+            dm |= 1u << s;
+        }
+        cur[s] = cand[s];
+    }
+    // running best (align.cpp:123-127): strict improvement, first cell wins
+    if (gmax - X > S.Tv) {
+        S.Tv = gmax - X;
+        S.best_d = d;
+        const unsigned bal = __ballot_sync(0xFFFFFFFFu, mv == gmax);
+        const int bl = 31 - __clz(bal);
+        const int bs = __shfl_sync(0xFFFFFFFFu, mk & 63, bl);
+        S.best_u = S.ubase + bl * SS + bs;
+    }
+    // live slots of row d (align.cpp:138-145)
+    S.hs2 = S.hs1;
+    S.lr2 = S.lr1;
+    {
+        const uint32_t lv = ~dm & vml;
+        const int hs_l = lv ? k0 + wbfind(lv) : -1;
+        const int ls_l = lv ? k0 + __ffs(lv) - 1 : kBig;
+        const int hs = __reduce_max_sync(0xFFFFFFFFu, hs_l);
+        const int ls = __reduce_min_sync(0xFFFFFFFFu, ls_l);
+        S.hs1 = hs;
+        S.lr1 = hs < 0 ? -1 : KB - ls;
+    }
+    wfeed<K, MODE, ODD>(S, lane);
+    S.d = d + 1;
+}
+
+// resident blocks per SM the register budget is sized for
+template <int K>
+constexpr int wide_min_blocks() {
+    return K <= 128 ? 6 : K <= 256 ? 4 : K <= 512 ? 2 : 1;
+}
+
+template <int K, int MODE>
+__global__ void __launch_bounds__(32 * kWideWarps, wide_min_blocks<K>()) wide_tier_kernel(TierParams P) {
+    using St = WState<K, MODE>;
+    constexpr int SS = St::S;
+    constexpr int KB = St::KB;
+    __shared__ tab_t tab[MODE == 0 ? 1 : kTabWords];
+    __shared__ int32_t rows[kWideWarps][K];  // recentring scratch, one row per warp
+    const int32_t gap = P.scheme->gap, X = P.scheme->x;
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int k0 = lane * SS;
+    Queue Q;
+    if (P.pilot || P.role == kRoleConsumer || !make_queue(P, Q) || Q.len == 0) return;
+    if constexpr (MODE != 0) {
+        tab_fill(tab, P.scheme, gap);
+        __syncthreads();
+    }
+    const int next_tier = (P.esc_to_warp || P.tier + 1 >= kWarpTier) ? kWarpTier : P.tier + 1;
+    WSink sk;
+    sk.esc_list = P.lists + (long long)next_tier * P.n_units;
+    sk.esc_len = &P.ctr->list_len[next_tier];
+    sk.units = sk.cells = sk.esc = 0;
+    sk.resumable = next_tier != kWarpTier;
+
+    St S;
+    int32_t E[SS], O[SS];
+    for (;;) {
+        // ---- next unit (warp-uniform) ----
+        unsigned long long i = Q.len;
+        // a plain read first: warps arriving after the queue ran dry leave
+        // without queueing on the cursor's atomic
+        if (lane == 0 && *(volatile unsigned long long*)Q.cursor < Q.len) i = atomicAdd(Q.cursor, 1ull);
+        i = __shfl_sync(0xFFFFFFFFu, i, 0);
+        if (i >= Q.len) break;
+        const uint32_t e = Q.q[(long long)i * Q.stride];
+        uint32_t unit = e;
+        const int32_t* rec = nullptr;
+        if (e & kResumeFlag) {
+            rec = record_ptr(P.resume, e);
+            unit = uint32_t(__ldcg(rec + kRecUnit));
+        }
+        const DevUnit u = P.units[unit];
+        if (u.route != 0) continue;  // guard failed: the warp tier's (prep listed it there)
+        S.unit = int32_t(unit);
+        S.h_pos = u.h_pos;
+        S.v_pos = u.v_pos;
+        S.m = u.h_len;
+        S.n = u.v_len;
+        S.hdir = u.dir & 1;
+        S.vdir = (u.dir >> 1) & 1;
+        S.stop = 0;
+        // per-unit refill schedule (the warp holds one unit): refills at the
+        // start of iterations PER, 2 PER, ...; each iteration consumes one v and
+        // one h symbol, so a fresh reader covers the PER symbols before the first
+        unsigned it = 0;
+        constexpr int PER = St::RPER;
+        if (!rec) {
+            S.d = 1;
+            S.ubase = -(K / 2);
+            S.hs1 = K / 2;
+            S.lr1 = KB - K / 2;
+            S.hs2 = S.lr2 = -1;
+            S.Tv = 1;  // T + beta d + 1 at d = 0, T = 0
+            S.best_d = S.best_u = 0;
+            S.delta_w = 1;
+            S.cells = 1;
+#pragma unroll
+            for (int s = 0; s < SS; ++s) {
+                O[s] = kDeadS;
+                E[s] = (k0 + s == K / 2) ? X + 1 : kDeadS;  // s(0,0) = 0 + 0 + off
+            }
+            w_limits(S);
+            w_windows(S, P.pool, lane, PER, PER);
+        } else {
+            // continue from a narrower tier's record, centred (see resume_unit)
+            const int ko = __ldcg(rec + kRecK);
+            const int off = (K - ko) >> 1;
+            const int d = __ldcg(rec + kRecD);
+            S.ubase = __ldcg(rec + kRecUbase) - off;
+            S.Tv = __ldcg(rec + kRecTc) >> 6;
+            S.best_d = __ldcg(rec + kRecBestD);
+            S.best_u = __ldcg(rec + kRecBestU);
+            S.cells = __ldcg(rec + kRecCells);
+            S.delta_w = __ldcg(rec + kRecDeltaW);
+            const int h1 = __ldcg(rec + kRecHs1), l1 = __ldcg(rec + kRecLs1);
+            const int h2 = __ldcg(rec + kRecHs2), l2 = __ldcg(rec + kRecLs2);
+            S.hs1 = h1 < 0 ? -1 : h1 + off;
+            S.lr1 = h1 < 0 ? -1 : KB - (l1 + off);
+            S.hs2 = h2 < 0 ? -1 : h2 + off;
+            S.lr2 = h2 < 0 ? -1 : KB - (l2 + off);
+            const bool odd = d & 1;
+#pragma unroll
+            for (int s = 0; s < SS; ++s) {
+                const int src = k0 + s - off;
+                const bool in = src >= 0 && src < ko;
+                const int32_t vc = in ? __ldcg(rec + kRecRows + src) : kDeadS;       // row d-2
+                const int32_t vp = in ? __ldcg(rec + kRecRows + ko + src) : kDeadS;  // row d-1
+                O[s] = odd ? vc : vp;
+                E[s] = odd ? vp : vc;
+            }
+            // the loop steps odd then even antidiagonals; a record at an even d
+            // runs its even step first, with the windows built at d-1 and fed v
+            S.d = odd ? d : d - 1;
+            w_windows(S, P.pool, lane, PER, PER);
+            S.d = d;
+            w_limits(S);
+            if (!odd) {
+                wfeed<K, MODE, true>(S, lane);
+                wstep<K, MODE, false>(S, E, O, P, tab, gap, X, it, lane, sk, rows[warp]);
+                if (!S.stop) w_windows(S, P.pool, lane, PER, PER);
+            }
+        }
+        // ---- the unit's antidiagonals, odd then even ----
+        while (!S.stop) {
+            if ((it & (PER - 1)) == 0 && it) {
+                if (lane == 0) S.rv.refill(P.pool);
+                if (lane == 31) S.rh.refill(P.pool);
+            }
+            wstep<K, MODE, true>(S, O, E, P, tab, gap, X, it, lane, sk, rows[warp]);
+            if (S.stop) break;
+            wstep<K, MODE, false>(S, E, O, P, tab, gap, X, it, lane, sk, rows[warp]);
+            ++it;
+        }
+    }
+    if (lane != 0) return;
+    if (sk.units) atomicAdd(&P.ctr->units[P.tier], sk.units);
+    if (sk.cells) atomicAdd(&P.ctr->cells[P.tier], sk.cells);
+    if (sk.esc) atomicAdd(&P.ctr->escalated[P.tier], sk.esc);
+}
+
+#define XB_WINST(K)                                                 \
+    template __global__ void wide_tier_kernel<K, 0>(TierParams);    \
+    template __global__ void wide_tier_kernel<K, 1>(TierParams);    \
+    template __global__ void wide_tier_kernel<K, 2>(TierParams);
+XB_WINST(128)
+XB_WINST(256)
+XB_WINST(512)
+XB_WINST(1024)
+#undef XB_WINST
+
+}  // namespace xb

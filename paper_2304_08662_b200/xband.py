@@ -465,6 +465,21 @@ def extend_tasks(pool: DevicePool, tasks, k: int, band: int, exec_flags: int = 0
     return out, ss
 
 
+def shard_tasks(pool: DevicePool, tasks, k: int, n_shards: int, locality: bool = False) -> np.ndarray:
+    """xb_shard_tasks: shard index (int32) of every task, one shard per GPU.
+    LPT on estimated cost, or locality-aware (a breadth-first sweep of the
+    sequence graph cut into equal-cost runs, so a shard references a compact
+    part of the pool, which is all its device uploads)."""
+    t = tasks_array(tasks)
+    out = np.zeros(len(t), dtype=np.int32)
+    bad = C.c_int64(-1)
+    rc = lib().xb_shard_tasks(pool._h, t.ctypes.data, len(t), k, n_shards,
+                              capi.XB_SHARD_LOCALITY if locality else capi.XB_SHARD_LPT,
+                              out.ctypes.data, C.byref(bad))
+    _raise(rc, "xb_shard_tasks", bad.value)
+    return out
+
+
 def extend_batches(batches, k: int, band: int, exec_flags: int = 0, n_devices: int = 1,
                    device_ids=None, reupload: bool = False, stats: list | None = None):
     """A stream of batches through the device-resident batch C-ABI

@@ -15,6 +15,7 @@ ap.add_argument("--config", type=int, default=5)
 ap.add_argument("--scale", type=float, default=0.05)
 ap.add_argument("--runs", type=int, default=2)
 ap.add_argument("--flags", type=int, default=0)
+ap.add_argument("--shard", default=None, help="i/N: only shard i of N (xb_shard_tasks, locality)")
 a = ap.parse_args()
 ds = synth.make(a.config, a.scale)
 if ds.cfg == 3:
@@ -23,7 +24,11 @@ else:
     s = xb.ScoringScheme.match_mismatch(1, -1, -1, ds.x)
 pool = xb.DevicePool(s, ds.symbols, ds.offsets)
 L = capi.lib()
-t = xb.xband.tasks_array(ds.tasks)
+tk = ds.tasks
+if a.shard:
+    i, n = (int(v) for v in a.shard.split("/"))
+    tk = tk[xb.xband.shard_tasks(pool, tk, ds.k, n, locality=True) == i]
+t = xb.xband.tasks_array(tk)
 ex = capi.make_exec(1, [0], None, a.flags)
 err, bad = C.c_int(0), C.c_int64(-1)
 b = L.xb_batch_create(pool._h, t.ctypes.data, len(t), ds.k, ds.band, C.byref(ex), C.byref(bad), C.byref(err))

@@ -57,11 +57,13 @@ def _by_scheme(entries):
 # 64 = NO_GROUP (one thread per unit), 32 = GROUP (lane groups throughout),
 # 8 | t << 8 = start at tier t without the pilot
 # 128 = THROUGHPUT (pilot + cost model even for a small batch)
+# 8 | t << 8 with t = 5..8: start on the wide tiers (one warp per unit, K128..K1024)
 TIER_FLAGS = ([0, 2, 128, 128 | 64] + [64 | 8 | (t << 8) for t in range(5)]
-              + [32 | 8 | (t << 8) for t in range(5)])
+              + [32 | 8 | (t << 8) for t in range(5)] + [8 | (t << 8) for t in range(5, 9)])
 TIER_IDS = (["auto", "warp_tier_only", "pilot_cascade", "thread_pilot_cascade"]
             + [f"thread_k{w}" for w in (16, 24, 32, 48, 64)]
-            + [f"group_k{w}" for w in (16, 24, 32, 48, 64)])
+            + [f"group_k{w}" for w in (16, 24, 32, 48, 64)]
+            + [f"wide_k{w}" for w in (128, 256, 512, 1024)])
 
 
 @pytest.mark.parametrize("flags", TIER_FLAGS, ids=TIER_IDS)
@@ -365,7 +367,7 @@ def test_route_guard_mixed_batch(xb, oracle):
     pool = xb.DevicePool(xb.ScoringScheme.match_mismatch(1, -2, -2, 10), sym, np.array(off))
     out = xb.extend_units(pool, units, band)
     st = xb.xband.last_stats()
-    assert st["units_tier"][5] == 2 and sum(st["units_tier"][:5]) == 3, st["units_tier"]
+    assert st["units_tier"][9] == 2 and sum(st["units_tier"][:9]) == 3, st["units_tier"]
     assert sum(st["escalated"]) == 0, st["escalated"]
     so = oracle.scheme_mm(1, -2, -2, 10)
     for q, (h, v) in enumerate(entries):
@@ -539,3 +541,106 @@ def test_pool_grows_after_upload(xb, oracle):
     check()
     grow(50)
     check()
+
+
+# Workloads whose live windows outgrow K64 (large X, low identity, the
+# reference's default band 1024): the wide tiers (one warp per unit, K128..
+# K1024, xb_wide.cu) carry them, entered from K64 escalations (resume
+# records from the thread, lane-group and pilot paths) or as the start tier.
+WIDE_CASES = {
+    "c4_x100": (4, 0.002, 100, 1024, "mm"),
+    "c2_x40": (2, 0.01, 40, 1024, "mm"),
+    "c5_x60_band512": (5, 0.0005, 60, 512, "mm"),
+    "c3_blosum_x80": (3, 0.01, 80, 1024, "blosum"),
+    "c4_x300_band200": (4, 0.001, 300, 200, "mm"),  # band failures inside the wide tiers
+}
+
+
+@pytest.mark.parametrize("case", sorted(WIDE_CASES))
+@pytest.mark.parametrize("flags", [0, 128, 32, 64 | 8, 8 | (5 << 8), 8 | (8 << 8), 16],
+                         ids=["auto", "pilot", "groups", "thread_k16", "wide_k128", "wide_k1024", "esc_to_warp"])
+def test_wide_tiers_vs_oracle(xb, oracle, case, flags):
+    from paper_2304_08662_b200 import synth
+    cfg, scale, x, band, kind = WIDE_CASES[case]
+    ds = synth.make(cfg, scale)
+    if kind == "blosum":
+        a, c = blosum62()
+        s = xb.ScoringScheme.from_matrix(xb.SubMatrix(a, c), -1, x)
+        os_ = oracle_scheme(oracle, ["BLOSUM62", -1, x])
+    else:
+        s = xb.ScoringScheme.match_mismatch(1, -1, -1, x)
+        os_ = oracle_scheme(oracle, [1, -1, -1, x])
+    pool = xb.DevicePool(s, ds.symbols, ds.offsets)
+    out, ss = xb.extend_tasks(pool, ds.tasks, ds.k, band, exec_flags=flags)
+    st = xb.xband.last_stats()
+    exp, ess = oracle.extend_batch(ds.symbols, ds.offsets, ds.tasks, ds.k, os_, band,
+                                   threads=os.cpu_count() or 1)
+    eq = result_rows_equal(out, exp)
+    assert eq.all(), f"{(~eq).sum()} of {len(eq)} sides differ; first {np.nonzero(~eq)[0][:5]}"
+    assert (ss == ess).all()
+    wide_units = sum(st["units_tier"][5:9])
+    if flags in (8 | (5 << 8), 8 | (8 << 8)):  # wide start: every thread-tier-routable unit is wide
+        assert sum(st["units_tier"][:5]) == 0 and wide_units > 0, st["units_tier"]
+    elif flags != 16 and (exp["delta_w"] > 66).any():  # windows beyond K64 (+ slack) reach the wide tiers
+        assert wide_units > 0, st["units_tier"]
+    if case == "c4_x300_band200":
+        assert (out["status"] == 1).any() and (out["status"] == 0).any()
+
+
+def test_wide_tier_is_the_start_for_wide_batches(xb):
+    """Throughput planning: when most of the pilot sample outgrows K64, the
+    whole batch starts on the wide tiers (no thread-tier pass first)."""
+    from paper_2304_08662_b200 import synth
+    ds = synth.make(4, 0.02)
+    s = xb.ScoringScheme.match_mismatch(1, -1, -1, 200)
+    pool = xb.DevicePool(s, ds.symbols, ds.offsets)
+    xb.extend_tasks(pool, ds.tasks, ds.k, 1024, exec_flags=128)
+    st = xb.xband.last_stats()
+    assert st["start_tier"] >= 5, st
+    assert sum(st["units_tier"][:5]) == 0 and sum(st["units_tier"][5:9]) > 0, st["units_tier"]
+
+
+def test_locality_shards_same_results(xb):
+    """Multi-device batches with locality-aware shards (XB_FLAG_LOCALITY):
+    each device uploads only the sequences its shard references; rows equal
+    the single-device run (two shards on one GPU here)."""
+    from paper_2304_08662_b200 import synth
+    ds = synth.make(5, 0.01)
+    s = xb.ScoringScheme.match_mismatch(1, -1, -1, ds.x)
+    pool = xb.DevicePool(s, ds.symbols, ds.offsets)
+    a, sa = xb.extend_tasks(pool, ds.tasks, ds.k, ds.band)
+    full_h2d = xb.xband.last_stats()["h2d_bytes"]
+    for locality in (False, True):
+        pool2 = xb.DevicePool(s, ds.symbols, ds.offsets)
+        b, sb = xb.extend_tasks(pool2, ds.tasks, ds.k, ds.band, n_devices=2, device_ids=[0, 0],
+                                exec_flags=8192 if locality else 0)
+        assert result_rows_equal(a, b).all() and (sa == sb).all()
+        h2d = xb.xband.last_stats()["h2d_bytes"]
+        if locality:  # the two shards together upload about one pool, not two
+            assert h2d < 1.4 * full_h2d, (h2d, full_h2d)
+
+
+def test_partial_residency_uploads_each_sequence_once(xb, oracle):
+    """A batch referencing a few sequences of a large pool uploads only their
+    words; a later batch over other sequences uploads the missing ones; the
+    rows equal the oracle's over the whole pool."""
+    from paper_2304_08662_b200 import synth
+    ds = synth.make(5, 0.02)
+    s = xb.ScoringScheme.match_mismatch(1, -1, -1, ds.x)
+    pool = xb.DevicePool(s, ds.symbols, ds.offsets)
+    image = (len(ds.symbols) + 2 * 4096) / 4
+    os_ = oracle_scheme(oracle, [1, -1, -1, ds.x])
+    rng = np.random.default_rng(3)
+    seen = np.zeros(len(ds.offsets) - 1, dtype=bool)
+    for rnd in range(3):
+        pick = np.sort(rng.choice(ds.n_tasks, size=150, replace=False))
+        t = ds.tasks[pick]
+        out, ss = xb.extend_tasks(pool, t, ds.k, ds.band)
+        h2d = xb.xband.last_stats()["h2d_bytes"]
+        ref = np.unique(np.concatenate([t[:, 0], t[:, 1]]))
+        new = ref[~seen[ref]]
+        seen[ref] = True
+        words = np.diff(ds.offsets)[new].sum() / 4
+        assert h2d < 150 * 32 + 16 * (len(ds.offsets) - 1) + 2 * words + 4096 + 0.02 * image, (rnd, h2d, words)
+        exp, ess = oracle.extend_batch(ds.symbols, ds.offsets, t, ds.k, os_, ds.band)
+        assert result_rows_equal(out, exp).all() and (ss == ess).all()
