@@ -48,14 +48,27 @@ $(OBJDIR)/xb_ingest.o: $(CSRC)/xb_ingest.cpp include/xdrop_b200.h
 
 $(LIB): $(OBJDIR)/xb_kernels.o $(OBJDIR)/xb_thread.o $(OBJDIR)/xb_group.o $(OBJDIR)/xb_wide.o $(OBJDIR)/xb_engine.o $(OBJDIR)/xb_synth.o $(OBJDIR)/xb_ingest.o
 	@mkdir -p $(dir $(LIB))
-	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^ -lpthread
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^ -lcudadevrt -lpthread
+
+# the bounds-checked variant (XB_CHECKS: every pool load, result row, list
+# slot, record and table lookup asserted; xb_debug_checks reads the first
+# failure): the GPU test-suite runs against it with XB_LIB_PATH
+CHK_LIB := paper_2304_08662_b200/_lib/libxdrop_b200_checked.so
+CHKDIR := build_chk
+checked: $(CHK_LIB)
+$(CHKDIR)/%.o: $(CSRC)/%.cu $(HDRS)
+	@mkdir -p $(CHKDIR)
+	$(NVCC) $(NVFLAGS) -DXB_CHECKS=1 -dc -o $@ $< > /dev/null 2>&1 || $(NVCC) $(NVFLAGS) -DXB_CHECKS=1 -dc -o $@ $<
+$(CHK_LIB): $(CHKDIR)/xb_kernels.o $(CHKDIR)/xb_thread.o $(CHKDIR)/xb_group.o $(CHKDIR)/xb_wide.o $(CHKDIR)/xb_engine.o $(OBJDIR)/xb_synth.o $(OBJDIR)/xb_ingest.o
+	@mkdir -p $(dir $(CHK_LIB))
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^ -lcudadevrt -lpthread
 
 oracle:
 	$(MAKE) -s -C oracle liboracle.so
 	@if [ -d /root/reference/proj/src ]; then $(MAKE) -s -C oracle ref; fi
 
 clean:
-	rm -rf $(OBJDIR) $(LIB)
+	rm -rf $(OBJDIR) $(LIB) $(CHKDIR) $(CHK_LIB)
 	$(MAKE) -C oracle clean
 
-.PHONY: all lib oracle clean
+.PHONY: all lib oracle clean checked

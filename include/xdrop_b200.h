@@ -201,6 +201,12 @@ int xb_last_stats(xb_stats* st);
 int xb_measure_int32_peak(int device, double* alu_ops_per_clk_sm, double* mixed_ops_per_clk_sm,
                           double* clk_mhz, int* sm_count);
 
+/* Checked builds only (make checked: -DXB_CHECKS=1, libxdrop_b200_checked.so):
+ * waits for `device`, returns in *failed the id of the first bounds check
+ * that failed since the last call (0: none) and clears it.  Product builds
+ * return -1 (checks compiled out). */
+int xb_debug_checks(int device, uint32_t* failed);
+
 /* ---- deterministic synthetic configs (BASELINE.json configs[0..4]) ---- */
 /* Builds config `cfg` (1..5) at `scale` (1.0 = the BASELINE size).  Returns
  * a handle; query sizes then copy out.  Matrix configs (cfg 3) take the

@@ -63,7 +63,7 @@ struct GState {
     int32_t Tc, best_d, best_u, cells, delta_w;
     uint32_t VW, HW;             // 2-bit windows of this lane's S slots (MODE 0)
     uint32_t VWb[NB], HWb[NB];   // byte windows (table modes)
-    static constexpr int RENC = MODE == 2 ? ENC_8BIT : ENC_2BIT;  // pool encoding read
+    static constexpr int RENC = MODE == 2 ? ENC_5BIT : ENC_2BIT;  // pool encoding read
     static constexpr int RPER = EncFields<RENC>::PER;              // refill period (iterations)
     Reader<true, RENC> rv;       // lane 0: v symbols entering slot 0
     Reader<false, RENC> rh;      // lane G-1: h symbols entering slot K-1
@@ -90,7 +90,7 @@ __device__ __forceinline__ void g_windows(GState<K, G, MODE>& S, const uint32_t*
         if (lane == 0) S.rv.init(pool, S.v_pos, S.vdir, a + 1, rv_r);
         if (lane == G - 1) S.rh.init(pool, S.h_pos, S.hdir, b + K, rh_r);
     } else {
-        constexpr int ENC = MODE == 1 ? ENC_2BIT : ENC_8BIT;
+        constexpr int ENC = MODE == 1 ? ENC_2BIT : ENC_5BIT;
 #pragma unroll
         for (int r = 0; r < GState<K, G, MODE>::NB; ++r) {
             uint32_t vw = 0, hw = 0;
@@ -251,6 +251,7 @@ __device__ __forceinline__ void gfinish(GState<K, G, MODE>& S, const TierParams&
         }
         if (lane == 0) {
             const unsigned long long slot = atomicAdd(sk.esc_len, 1ull);
+            XB_ASSERT(slot < P.ck_units, kChkList);
             sk.esc_list[slot] = entry;
             ++sk.esc;
         }
@@ -272,6 +273,7 @@ __device__ __forceinline__ void gfinish(GState<K, G, MODE>& S, const TierParams&
         res.status = kStatusOk;
         res.spread = 0;
     }
+    XB_ASSERT((unsigned long long)S.unit < P.ck_units, kChkResult);
     P.results[S.unit] = res;
     ++sk.units;
     sk.cells += (unsigned long long)S.cells;
@@ -649,6 +651,7 @@ __global__ void __launch_bounds__(128) group_tier_kernel(TierParams P) {
                     S.m = S.n = 0;
                     return;
                 }
+                XB_ASSERT(i * Q.stride < P.ck_units, kChkList);
                 e = Q.q[(long long)i * Q.stride];
             }
             uint32_t unit = e;
@@ -657,6 +660,7 @@ __global__ void __launch_bounds__(128) group_tier_kernel(TierParams P) {
                 rec = record_ptr(P.resume, e);
                 unit = uint32_t(__ldcg(rec + kRecUnit));
             }
+            XB_ASSERT(unit < P.ck_units, kChkUnit);
             const DevUnit u = P.units[unit];
             if (u.route != 0) {
                 if (P.pilot && lane == 0) P.pilot_w[i] = -2;

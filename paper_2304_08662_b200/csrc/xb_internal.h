@@ -6,9 +6,11 @@
 namespace xb {
 
 // Pool encodings. ENC_2BIT: pure ACGT, codes A0 C1 G2 T3, 16 symbols per
-// 32-bit word. ENC_8BIT: alphabet index (< 32) in a byte, 4 per word, so a
-// view streams through the same aligned-chunk readers as 2-bit DNA.
-enum : int { ENC_2BIT = 2, ENC_8BIT = 8 };
+// 32-bit word. ENC_5BIT: alphabet index (< 32, 31 = the sentinel) in 5 bits,
+// symbol p at bits [5p, 5p+5) of the word stream (protein, DNA with N): 5/8
+// of a byte pool.  The kernels' readers unpack 4 symbols at a time into byte
+// codes, so the table modes see the same byte windows either way.
+enum : int { ENC_2BIT = 2, ENC_5BIT = 5 };
 
 // symbols of zero padding in front of / behind every device pool, so window
 // fetches that run past a sequence (masked out later) never leave the buffer
@@ -100,6 +102,9 @@ enum : int {
 // the record an escalation-list entry with kResumeFlag points at
 XB_HD inline int32_t* record_ptr(int32_t* resume, uint32_t e) {
     const int64_t i = int64_t(e & kResumeIndex);
+#if defined(XB_CHECKS) && XB_CHECKS && defined(__CUDA_ARCH__)
+    if (i >= ((e & kResumeWideFlag) ? kResumeWideCap : kResumeCap)) return nullptr;  // faults loudly
+#endif
     return (e & kResumeWideFlag) ? resume + int64_t(kResumeCap) * kResumeStride + i * kResumeWideStride
                                  : resume + i * kResumeStride;
 }

@@ -8,6 +8,20 @@
 
 namespace xb {
 
+#if XB_CHECKS
+__device__ PoolRange xb_pool_ranges[kCheckPools];
+__device__ unsigned int xb_check_fail;
+// a pool-word load must fall inside the registered image its base points into
+__device__ __noinline__ bool pool_load_ok(const uint32_t* pool, int64_t wi) {
+    const uint32_t* a = pool + wi;
+    for (int r = 0; r < kCheckPools; ++r) {
+        const PoolRange e = xb_pool_ranges[r];
+        if (e.base && pool >= e.base && pool < e.base + e.words) return a >= e.base && a < e.base + e.words;
+    }
+    return false;
+}
+#endif
+
 // ------------------------------------------------------------- helpers ----
 
 // contiguous bit range [lo, hi] of a 32-bit word, lo/hi already clamped to
@@ -40,6 +54,7 @@ __global__ void __launch_bounds__(128) warp_tier_kernel(TierParams P) {
     const int lane = threadIdx.x & 31;
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int band = P.band;
+    XB_ASSERT((unsigned long long)gw < P.ck_warp_slots, kChkScratch);
     int32_t* rows0 = P.warp_scratch + int64_t(gw) * 2 * band;
     int32_t* rows1 = rows0 + band;
     const int32_t gap = P.scheme->gap, X = P.scheme->x;
@@ -52,7 +67,9 @@ __global__ void __launch_bounds__(128) warp_tier_kernel(TierParams P) {
         if (lane == 0) q = atomicAdd(&P.ctr->cursor[kWarpTier], 1ull);
         q = __shfl_sync(0xFFFFFFFFu, q, 0);
         if (q >= qlen) break;
+        XB_ASSERT(q < P.ck_units, kChkList);
         const uint32_t unit = queue[q];
+        XB_ASSERT(unit < P.ck_units, kChkUnit);
         const DevUnit U = P.units[unit];
         const int m = U.h_len, n = U.v_len;
 
@@ -177,6 +194,7 @@ __global__ void __launch_bounds__(128) warp_tier_kernel(TierParams P) {
             res.cells = cells;
             res.status = status;
             res.spread = spread;
+            XB_ASSERT(unit < P.ck_units, kChkResult);
             P.results[unit] = res;
             ++my_units;
             my_cells += (unsigned long long)cells;
@@ -190,7 +208,7 @@ __global__ void __launch_bounds__(128) warp_tier_kernel(TierParams P) {
 }
 
 template __global__ void warp_tier_kernel<ENC_2BIT>(TierParams);
-template __global__ void warp_tier_kernel<ENC_8BIT>(TierParams);
+template __global__ void warp_tier_kernel<ENC_5BIT>(TierParams);
 
 // ----------------------------------------------------------------- prep ----
 // LR split (partition.cpp:45-81) + checked seed score (align.cpp:283-285)
@@ -238,8 +256,8 @@ __global__ void prep_kernel(PrepParams P) {
             hc = code_at<ENC_2BIT>(P.pool, hb + hs, 1, 1ll << 40, i);
             vc = code_at<ENC_2BIT>(P.pool, vb + vs, 1, 1ll << 40, i);
         } else {
-            hc = code_at<ENC_8BIT>(P.pool, hb + hs, 1, 1ll << 40, i);
-            vc = code_at<ENC_8BIT>(P.pool, vb + vs, 1, 1ll << 40, i);
+            hc = code_at<ENC_5BIT>(P.pool, hb + hs, 1, 1ll << 40, i);
+            vc = code_at<ENC_5BIT>(P.pool, vb + vs, 1, 1ll << 40, i);
         }
         ss += P.scheme->sim[hc * 32 + vc];  // sim(h symbol, v symbol)
     }

@@ -32,7 +32,39 @@
 
 #include "xb_internal.h"
 
+// Checked builds (make checked, -DXB_CHECKS=1: the bounds-asserting
+// library the GPU test-suite also runs against, in place of compute-
+// sanitizer, which this pool does not offer): every pool-word load, result
+// row, escalation-list slot, resume record and table lookup is checked
+// against its buffer; the first failed check's id is kept for the host
+// (xb_debug_checks).  Product builds compile the checks away.
+#ifndef XB_CHECKS
+#define XB_CHECKS 0
+#endif
+
 namespace xb {
+
+#if XB_CHECKS
+// pool images resident on this device (registered by the host when it
+// allocates them): a pool-word load must fall inside the image it reads
+struct PoolRange {
+    const uint32_t* base;
+    unsigned long long words;
+};
+constexpr int kCheckPools = 32;
+extern __device__ PoolRange xb_pool_ranges[kCheckPools];
+extern __device__ unsigned int xb_check_fail;  // first failed check id (0: none)
+__device__ __noinline__ bool pool_load_ok(const uint32_t* pool, int64_t wi);  // xb_kernels.cu
+#define XB_ASSERT(cond, id)                                          \
+    do {                                                             \
+        if (!(cond)) atomicCAS(&xb::xb_check_fail, 0u, (unsigned)(id)); \
+    } while (0)
+#else
+#define XB_ASSERT(cond, id) ((void)0)
+#endif
+enum : unsigned {  // check ids
+    kChkPool = 1, kChkResult, kChkList, kChkRecord, kChkTable, kChkUnit, kChkScratch, kChkSmemRow
+};
 
 constexpr int32_t kDeadS = -(1 << 24);  // dead sentinel in drift space
 
@@ -48,6 +80,7 @@ constexpr int kTabPitch = 33;
 constexpr int kTabWords = 32 * kTabPitch;
 __device__ __forceinline__ int32_t tab_lookup(const tab_t* __restrict__ tab, uint32_t vh_bytes) {
     const uint32_t off = __dp4a(vh_bytes, 4u | (4u * kTabPitch) << 8, 0u);
+    XB_ASSERT(off < 4u * kTabWords, kChkTable);
     return *reinterpret_cast<const tab_t*>(reinterpret_cast<const char*>(tab) + off);
 }
 // fills the table (all threads of the block, then the caller syncs)
@@ -106,6 +139,10 @@ struct TierParams {
     int32_t two;                         // 2
     uint32_t ones;                       // 0x01010101
     uint32_t mulc[16];                   // 2^(32-2f), f = 1..15
+#if XB_CHECKS
+    unsigned long long ck_units;         // result rows = list slots per tier
+    unsigned long long ck_warp_slots;    // warp-tier scratch slots
+#endif
 };
 // The K24 loop re-reads these constants from the parameter bank; with r64 at
 // an offset = 4 (mod 8) ptxas pairs them so that the loop runs 165 ms on full
@@ -115,6 +152,7 @@ static_assert(offsetof(TierParams, r64) % 8 == 4, "keep the opaque constants' pa
 // ---------------------------------------------------------------- pool ----
 
 __device__ __forceinline__ uint32_t ldw(const uint32_t* __restrict__ pool, int64_t wi) {
+    XB_ASSERT(pool_load_ok(pool, wi), kChkPool);
     return __ldg(pool + wi);
 }
 
@@ -147,18 +185,21 @@ __device__ __forceinline__ uint32_t code_at(const uint32_t* __restrict__ pool, i
     if (t < 0 || t >= len) return kSentinel;
     const int64_t p = dir ? pos + t : pos - t;
     if (ENC == ENC_2BIT) return (ldw(pool, p >> 4) >> (uint32_t(p & 15) * 2u)) & 3u;
-    return (ldw(pool, p >> 2) >> (uint32_t(p & 3) * 8u)) & 0xFFu;
+    const int64_t b = 5 * p;  // 5-bit stream
+    return __funnelshift_r(ldw(pool, b >> 5), ldw(pool, (b >> 5) + 1), uint32_t(b & 31)) & 31u;
 }
 
-// field geometry of an encoding: PER symbols of BITS bits per 32-bit word
+// Field geometry of a reader's chunk: PER symbols of BITS bits per 32-bit
+// word.  5-bit pools are read as byte codes: a chunk is 4 symbols unpacked
+// from 20 stream bits into 4 bytes (the table modes' window layout).
 template <int ENC>
 struct EncFields {
-    static constexpr int BITS = ENC == ENC_2BIT ? 2 : 8;
+    static constexpr int BITS = ENC == ENC_2BIT ? 2 : 8;  // bits per symbol in a chunk word
     static constexpr int PER = 32 / BITS;
     static constexpr int LOG = ENC == ENC_2BIT ? 4 : 2;
 };
 
-// exact reversal of the fields of a word
+// exact reversal of the fields of a chunk word
 template <int ENC>
 __device__ __forceinline__ uint32_t rev_fields(uint32_t x) {
     if constexpr (ENC == ENC_2BIT)
@@ -167,21 +208,34 @@ __device__ __forceinline__ uint32_t rev_fields(uint32_t x) {
         return __byte_perm(x, 0u, 0x0123);
 }
 
+// four 5-bit fields (bits 0-19) -> four bytes
+__device__ __forceinline__ uint32_t unpack5(uint32_t x) {
+    return (x & 0x1Fu) | ((x << 3) & 0x1F00u) | ((x << 6) & 0x1F0000u) | ((x << 9) & 0x1F000000u);
+}
+
 // PER symbols starting at pool symbol position q, lowest address in field 0
 template <int ENC>
 __device__ __forceinline__ uint32_t chunk_mem_e(const uint32_t* __restrict__ pool, int64_t q) {
-    using F = EncFields<ENC>;
-    const int64_t wi = q >> F::LOG;
-    const uint32_t sh = uint32_t(q & (F::PER - 1)) * uint32_t(F::BITS);
-    return __funnelshift_r(ldw(pool, wi), ldw(pool, wi + 1), sh);
+    if constexpr (ENC == ENC_5BIT) {
+        const int64_t b = 5 * q;
+        return unpack5(__funnelshift_r(ldw(pool, b >> 5), ldw(pool, (b >> 5) + 1), uint32_t(b & 31)));
+    } else {
+        using F = EncFields<ENC>;
+        const int64_t wi = q >> F::LOG;
+        const uint32_t sh = uint32_t(q & (F::PER - 1)) * uint32_t(F::BITS);
+        return __funnelshift_r(ldw(pool, wi), ldw(pool, wi + 1), sh);
+    }
 }
 
 // Streams consecutive PER-symbol chunks of a view.  Refills happen at
-// warp-uniform loop iterations (every PER: 16 for 2-bit, 4 for bytes), so no
-// thread diverges for them: `cur` is filled at (re)initialisation with the
-// symbols needed up to the next refill point, and each refill assembles the
-// chunk whose words were loaded one refill earlier.  TOP = chunks top-first
-// (v side: consume from the top field), else bottom-first (h side).
+// warp-uniform loop iterations (every PER: 16 for 2-bit, 4 for 5-bit pools),
+// so no thread diverges for them: `cur` is filled at (re)initialisation with
+// the symbols needed up to the next refill point, and each refill assembles
+// the chunk whose words were loaded one refill earlier.  TOP = chunks
+// top-first (v side: consume from the top field), else bottom-first (h side).
+// A 5-bit pool's chunk is 20 stream bits at a bit offset `sh` into (w0, w1);
+// each refill moves 20 bits on, and loads the next word (needed one refill
+// later) only when the chunk crosses a word boundary.
 // PF: hold one more word (`pend`), loaded a whole refill period before it is
 // first read, so no refill waits on a load; without it, the word loaded at a
 // refill is consumed right there (one register fewer, for the K <= 24 thread
@@ -207,6 +261,14 @@ struct Reader {
             cur = (TOP ? (d != 0) : (d == 0)) ? rev_fields<ENC>(c) : c;
         }
         const int64_t q = d ? pos + t0 + r : pos - (t0 + r) - (F::PER - 1);
+        if constexpr (ENC == ENC_5BIT) {
+            const int64_t b = 5 * q, wi = b >> 5;
+            sh = uint32_t(b & 31);
+            w0 = ldw(pool, wi);
+            w1 = ldw(pool, wi + 1);
+            wnext = d ? wi + 2 : wi - 1;
+            return;
+        }
         const int64_t wi = q >> F::LOG;
         sh = uint32_t(q & (F::PER - 1)) * uint32_t(F::BITS);
         w0 = ldw(pool, wi);
@@ -219,6 +281,27 @@ struct Reader {
         }
     }
     __device__ __forceinline__ void refill(const uint32_t* pool) {
+        if constexpr (ENC == ENC_5BIT) {
+            const uint32_t c = unpack5(__funnelshift_r(w0, w1, sh));
+            cur = (TOP ? (dir != 0) : (dir == 0)) ? rev_fields<ENC>(c) : c;
+            if (dir != 0) {  // forward: 20 bits on
+                sh += 20u;
+                if (sh >= 32u) {
+                    sh -= 32u;
+                    w0 = w1;
+                    w1 = ldw(pool, wnext++);
+                }
+            } else {         // backward: 20 bits back
+                if (sh >= 20u) {
+                    sh -= 20u;
+                } else {
+                    sh += 12u;
+                    w1 = w0;
+                    w0 = ldw(pool, wnext--);
+                }
+            }
+            return;
+        }
         const uint32_t c = __funnelshift_r(w0, w1, sh);
         const bool rev = TOP ? (dir != 0) : (dir == 0);
         cur = rev ? rev_fields<ENC>(c) : c;
@@ -275,7 +358,7 @@ struct TState {
     // windows
     uint32_t VW[MODE == 0 ? NW : NB];
     uint32_t HW[MODE == 0 ? NW : NB];
-    static constexpr int RENC = MODE == 2 ? ENC_8BIT : ENC_2BIT;  // pool encoding read
+    static constexpr int RENC = MODE == 2 ? ENC_5BIT : ENC_2BIT;  // pool encoding read
     static constexpr int RPER = EncFields<RENC>::PER;              // refill period (iterations)
     static constexpr bool RPF = K >= 32 && MODE == 0;  // register headroom for the prefetched word
     Reader<true, RENC, RPF> rv;

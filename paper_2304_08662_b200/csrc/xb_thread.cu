@@ -66,7 +66,7 @@ __device__ __forceinline__ void init_windows(TState<K, MODE>& S, const uint32_t*
         S.rv.init(pool, S.v_pos, S.vdir, a + 1, rv_r);
         S.rh.init(pool, S.h_pos, S.hdir, b + St::WK, rh_r);
     } else {
-        constexpr int ENC = MODE == 1 ? ENC_2BIT : ENC_8BIT;
+        constexpr int ENC = MODE == 1 ? ENC_2BIT : ENC_5BIT;
 #pragma unroll
         for (int r = 0; r < St::NB; ++r) {
             uint32_t vw = 0, hw = 0;
@@ -377,6 +377,7 @@ __device__ __forceinline__ void finish_unit(TState<K, MODE>& S, const TierParams
         // the record first, then the slot, then the entry (volatile)
         __threadfence();
         const unsigned long long slot = atomicAdd(sk.esc_len, 1ull);
+        XB_ASSERT(slot < P.ck_units, kChkList);
         *(volatile uint32_t*)&sk.esc_list[slot] = entry;
         ++sk.esc;
         return;
@@ -398,6 +399,7 @@ __device__ __forceinline__ void finish_unit(TState<K, MODE>& S, const TierParams
         res.status = kStatusOk;
         res.spread = 0;
     }
+    XB_ASSERT((unsigned long long)S.unit < P.ck_units, kChkResult);
     P.results[S.unit] = res;
     ++sk.units;
     sk.cells += (unsigned long long)S.cells;
@@ -630,6 +632,7 @@ __global__ void __launch_bounds__(kTB, tier_min_blocks<K, MODE>()) thread_tier_k
                 rec = record_ptr(P.resume, e);
                 unit = uint32_t(rec[kRecUnit]);
             }
+            XB_ASSERT(unit < P.ck_units, kChkUnit);
             // units whose values could leave the drift-space range go to the warp tier
             if (P.units[unit].route != 0) {
                 if (P.pilot) P.pilot_w[sk.qidx] = -2;  // not a thread-tier unit

@@ -65,7 +65,7 @@ struct WState {
     int32_t best_d, best_u, cells, delta_w;
     uint32_t VW[NW], HW[NW];     // 2-bit windows of this lane's S slots (MODE 0)
     uint32_t VWb[NB], HWb[NB];   // byte windows (table modes)
-    static constexpr int RENC = MODE == 2 ? ENC_8BIT : ENC_2BIT;
+    static constexpr int RENC = MODE == 2 ? ENC_5BIT : ENC_2BIT;
     static constexpr int RPER = EncFields<RENC>::PER;
     Reader<true, RENC> rv;       // lane 0: v symbols entering slot 0
     Reader<false, RENC> rh;      // lane 31: h symbols entering slot K-1
@@ -98,7 +98,7 @@ __device__ __forceinline__ void w_windows(WState<K, MODE>& S, const uint32_t* __
             S.HW[w] = chunk_bf(pool, S.h_pos, S.hdir, b + k0 + 16 * w) & keep;
         }
     } else {
-        constexpr int ENC = MODE == 1 ? ENC_2BIT : ENC_8BIT;
+        constexpr int ENC = MODE == 1 ? ENC_2BIT : ENC_5BIT;
 #pragma unroll
         for (int r = 0; r < St::NB; ++r) {
             uint32_t vw = 0, hw = 0;
@@ -150,6 +150,7 @@ __device__ __forceinline__ void w_shift(int32_t (&R)[SS], int sh, int lane, int3
         const int src = lane * SS + s + sh;
         R[s] = (src >= 0 && src < KK) ? row[src] : kDeadS;
     }
+    XB_ASSERT(sh > -KK && sh < KK, kChkSmemRow);
     __syncwarp();
 }
 
@@ -257,6 +258,7 @@ __device__ __forceinline__ void wfinish(WState<K, MODE>& S, const TierParams& P,
         if (lane == 0) {
             __threadfence();
             const unsigned long long slot = atomicAdd(sk.esc_len, 1ull);
+            XB_ASSERT(slot < P.ck_units, kChkList);
             sk.esc_list[slot] = entry;
             ++sk.esc;
         }
@@ -278,6 +280,7 @@ __device__ __forceinline__ void wfinish(WState<K, MODE>& S, const TierParams& P,
         res.status = kStatusOk;
         res.spread = 0;
     }
+    XB_ASSERT((unsigned long long)S.unit < P.ck_units, kChkResult);
     P.results[S.unit] = res;
     ++sk.units;
     sk.cells += (unsigned long long)S.cells;
@@ -511,6 +514,7 @@ __global__ void __launch_bounds__(32 * kWideWarps, wide_min_blocks<K>()) wide_ti
         if (lane == 0 && *(volatile unsigned long long*)Q.cursor < Q.len) i = atomicAdd(Q.cursor, 1ull);
         i = __shfl_sync(0xFFFFFFFFu, i, 0);
         if (i >= Q.len) break;
+        XB_ASSERT(i * Q.stride < P.ck_units, kChkList);
         const uint32_t e = Q.q[(long long)i * Q.stride];
         uint32_t unit = e;
         const int32_t* rec = nullptr;
@@ -518,6 +522,7 @@ __global__ void __launch_bounds__(32 * kWideWarps, wide_min_blocks<K>()) wide_ti
             rec = record_ptr(P.resume, e);
             unit = uint32_t(__ldcg(rec + kRecUnit));
         }
+        XB_ASSERT(unit < P.ck_units, kChkUnit);
         const DevUnit u = P.units[unit];
         if (u.route != 0) continue;  // guard failed: the warp tier's (prep listed it there)
         S.unit = int32_t(unit);

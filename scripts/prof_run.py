@@ -16,8 +16,14 @@ ap.add_argument("--scale", type=float, default=0.05)
 ap.add_argument("--runs", type=int, default=2)
 ap.add_argument("--flags", type=int, default=0)
 ap.add_argument("--shard", default=None, help="i/N: only shard i of N (xb_shard_tasks, locality)")
+ap.add_argument("--x", type=int, default=None)
+ap.add_argument("--band", type=int, default=None)
 a = ap.parse_args()
 ds = synth.make(a.config, a.scale)
+if a.x is not None:
+    ds.x = a.x
+if a.band is not None:
+    ds.band = a.band
 if ds.cfg == 3:
     s = xb.ScoringScheme.from_matrix(xb.parse_submatrix(synth.blosum62_text()), -1, ds.x)
 else:

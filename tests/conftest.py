@@ -40,3 +40,18 @@ def golden_dir():
 def has_gpu():
     from paper_2304_08662_b200 import capi
     return capi.lib().xb_device_count() > 0
+
+
+@pytest.fixture(autouse=True)
+def _bounds_checks(request):
+    """With XB_LIB_PATH pointing at the checked library (make checked), every
+    GPU test also asserts that no device-side bounds check failed."""
+    yield
+    if "gpu" not in request.keywords or "checked" not in os.environ.get("XB_LIB_PATH", ""):
+        return
+    import ctypes
+    from paper_2304_08662_b200 import capi
+    failed = ctypes.c_uint32(0)
+    rc = capi.lib().xb_debug_checks(0, ctypes.byref(failed))
+    assert rc == 0, "XB_LIB_PATH names a library without checks"
+    assert failed.value == 0, f"device bounds check {failed.value} failed (xb_kernels.cuh kChk* ids)"

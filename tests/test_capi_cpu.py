@@ -58,7 +58,7 @@ def test_pool_packing_choice_and_validation():
     p = xb.DevicePool(s, b"ACGTACGT", np.array([0, 4, 8]))
     assert p.bits_per_symbol == 2
     p2 = xb.DevicePool(s, b"ACGNACGT", np.array([0, 4, 8]))
-    assert p2.bits_per_symbol == 8
+    assert p2.bits_per_symbol == 5
     with pytest.raises(xb.UnknownSymbol):
         xb.DevicePool(s, b"ACGUACGT", np.array([0, 4, 8]))
     with pytest.raises(xb.UnknownSymbol):
@@ -155,7 +155,7 @@ def test_pool_packs_incrementally():
     assert p.add("ACGTACGT" * 1000) == 2
     assert p.bits_per_symbol == 2
     assert p.add("ACNGT") == 3
-    assert p.bits_per_symbol == 8
+    assert p.bits_per_symbol == 5
     assert p.add("T") == 4
     assert xb.capi.lib().xb_pool_size(p._h) == 5
     assert xb.capi.lib().xb_pool_seq_len(p._h, 3) == 5
@@ -163,7 +163,7 @@ def test_pool_packs_incrementally():
         p.add("ACGX")
     m = xb.ScoringScheme.from_matrix(xb.SubMatrix("AB", [2, -1, -1, 3]), -1, 4)
     q = xb.DevicePool(m, b"ABBA", np.array([0, 4], dtype=np.int64))
-    assert q.bits_per_symbol == 8
+    assert q.bits_per_symbol == 5
 
 
 def test_package_blosum62_matches_reference_fixture():

@@ -409,7 +409,7 @@ def test_table_modes_at_throughput_scale(xb, oracle, case):
         s = xb.ScoringScheme.from_matrix(xb.parse_submatrix(synth.blosum62_text()), -1, ds.x)
         so = oracle_scheme(oracle, ["BLOSUM62", -1, ds.x])
     pool = xb.DevicePool(s, ds.symbols, ds.offsets)
-    assert pool.bits_per_symbol == (2 if case == "dna_table_2bit" else 8)
+    assert pool.bits_per_symbol == (2 if case == "dna_table_2bit" else 5)
     out, ss = xb.extend_tasks(pool, ds.tasks, ds.k, ds.band, exec_flags=128 | 64)  # THROUGHPUT, threads
     st = xb.xband.last_stats()
     assert not st["start_lane_groups"]
@@ -482,7 +482,7 @@ def test_edge_batches(xb, oracle):
     sn = np.frombuffer("".join(seqs_n).encode(), dtype=np.uint8)
     on = np.cumsum([0] + [len(x) for x in seqs_n]).astype(np.int64)
     pn = xb.DevicePool(s, sn, on)
-    assert pn.bits_per_symbol == 8
+    assert pn.bits_per_symbol == 5
     tn = np.array([[0, 1, 200, 200], [1, 0, 10, 10], [0, 0, 60, 60]], dtype=np.int64)
     o2, s2 = xb.extend_tasks(pn, tn, k, 64)
     e2, es2 = oracle.extend_batch(sn, on, tn, k, so, 64, threads=1)
@@ -537,7 +537,7 @@ def test_pool_grows_after_upload(xb, oracle):
     grow(300)                 # far more words than the first upload held
     check()
     grow(5, "ACGTN")          # first N: the image widens to byte codes (4x the words)
-    assert pool.bits_per_symbol == 8
+    assert pool.bits_per_symbol == 5
     check()
     grow(50)
     check()

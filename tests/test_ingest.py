@@ -159,6 +159,6 @@ def test_pool_from_fasta_equals_pool_from_buffers():
     text = ">a\nACGTACGT\n>b\nacgtnn\n"
     s = xb.ScoringScheme.match_mismatch(1, -1, -1, 5)
     p = xb.DevicePool.from_fasta(text, s)
-    assert p.n == 2 and p.bits_per_symbol == 8  # N present: byte pool
+    assert p.n == 2 and p.bits_per_symbol == 5  # N present: 5-bit codes
     p2 = xb.DevicePool.from_fasta(">a\nACGT\n", s)
     assert p2.bits_per_symbol == 2
