@@ -1811,7 +1811,7 @@ int xb_batch_stats(xb_batch* B, xb_stats* st) {
         CK(cudaStreamSynchronize(D.stream));
         std::memcpy(&c, D.h_misc, sizeof c);
         float ms[3 + kNumTiers] = {0};
-        if (D.n_units) {
+        if (D.n_units && B->ran) {  // before the first run no event has been recorded
             CK(cudaEventElapsedTime(&ms[0], D.ev[kEvStart], D.ev[kEvWarp]));  // whole run
             CK(cudaEventElapsedTime(&ms[1], D.ev[kEvStart], D.ev[kEvPrep]));  // prep + sort
             CK(cudaEventElapsedTime(&ms[2], D.ev[kEvPrep], D.ev[kEvPilot]));  // pilot + select
