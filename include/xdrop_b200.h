@@ -79,7 +79,7 @@ typedef struct {
 
 #define XB_FLAG_NO_SORT 1       /* skip the longest-first cost sort (ablation) */
 #define XB_FLAG_GENERIC_ONLY 2  /* route every unit to the warp tier (testing) */
-#define XB_FLAG_FORCE_TIER 8    /* start at thread tier (flags >> 8) & 15, no pilot (testing) */
+#define XB_FLAG_FORCE_TIER 8    /* start at tier (flags >> 8) & 15, no pilot (testing) */
 #define XB_FLAG_ESC_TO_WARP 16  /* units outgrowing the start tier go straight to the warp tier */
 #define XB_FLAG_GROUP 32        /* every thread-tier launch runs as lane groups (testing) */
 #define XB_FLAG_NO_GROUP 64     /* never use lane groups: one thread per unit throughout (ablation) */
@@ -89,10 +89,11 @@ typedef struct {
 
 /* Per-call device statistics (summed over devices; times are the max).
  * Tiers: 0..4 = one unit per thread (or per 4-lane group) with a
- * K = 16/24/32/48/64 slot register band; 5..8 = one warp per unit with a
- * K = 128/256/512/1024 slot register band; 9 = one warp per unit, rows in
- * global memory (exact generic path, any band). */
-#define XB_NUM_TIERS 10
+ * K = 16/24/32/48/64 slot register band; 5..9 = 8-32 lanes per unit with a
+ * K = 96/128/256/512/1024 slot register band; 10 = one warp per unit, rows
+ * in global memory (exact generic path, any band).  Tiers after the start
+ * tier are dispatched on the device; their time is reported as tier 10's. */
+#define XB_NUM_TIERS 11
 typedef struct {
     int32_t n_devices;
     int32_t launches;            /* kernels launched by the last run */

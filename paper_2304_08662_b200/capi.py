@@ -62,13 +62,12 @@ class XbExec(C.Structure):
                 ("stream", C.c_void_p), ("flags", C.c_int32)]
 
 
-# tiers 0-4: thread / lane-group register bands; 5-8: wide (one warp per unit); 9: warp tier
-TIER_NAMES = ["thread_k16", "thread_k24", "thread_k32", "thread_k48", "thread_k64",
-              "wide_k128", "wide_k256", "wide_k512", "wide_k1024", "warp"]
-TIER_WIDTHS = [16, 24, 32, 48, 64, 128, 256, 512, 1024]
+# tiers 0-4: thread / lane-group register bands; 5-9: wide (8-32 lanes per unit); 10: warp tier
+TIER_WIDTHS = [16, 24, 32, 48, 64, 96, 128, 256, 512, 1024]
+TIER_NAMES = [f"thread_k{w}" for w in TIER_WIDTHS[:5]] + [f"wide_k{w}" for w in TIER_WIDTHS[5:]] + ["warp"]
 NUM_TIERS = len(TIER_NAMES)
 WIDE_FIRST = 5
-WARP_TIER = 9
+WARP_TIER = NUM_TIERS - 1
 
 
 def tier_kernel_name(t: int, stats: dict, flags: int = 0) -> str:

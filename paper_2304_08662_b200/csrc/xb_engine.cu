@@ -30,7 +30,7 @@ template <int K, int MODE>
 __global__ void thread_tier_kernel(TierParams P);
 template <int K, int G, int MODE>
 __global__ void group_tier_kernel(TierParams P);
-template <int K, int MODE>
+template <int K, int G, int MODE>
 __global__ void wide_tier_kernel(TierParams P);
 template <int ENC>
 __global__ void warp_tier_kernel(TierParams P);
@@ -710,7 +710,7 @@ constexpr int kMiscStartTier = 1000;
 // (fetch), the cascade-order marker, and the early result copy.
 enum : int { kEvStart = 0, kEvPrep = 1, kEvPilot = 2, kEvTier = 3, kEvWarp = kEvTier + kWarpTier,
              kEvFetch, kEvOrder, kEvCopy, kNumEv };
-static_assert(kNumEv <= 16, "Workspace::ev");
+static_assert(kNumEv <= 20, "Workspace::ev");
 
 struct Workspace {
     int dev = 0;
@@ -718,7 +718,7 @@ struct Workspace {
     int64_t capU = 0, capI = 0;
     size_t scratch_bytes = 0, cub_bytes = 0;
     cudaStream_t stream = nullptr;
-    cudaEvent_t ev[16] = {};  // kEv* below
+    cudaEvent_t ev[20] = {};  // kEv* below
     int64_t* d_tasks = nullptr;
     DevUnit* d_units = nullptr;
     uint32_t *d_keys = nullptr, *d_vals = nullptr, *d_keys2 = nullptr, *d_order = nullptr;
@@ -828,7 +828,7 @@ struct DevBatch {
     cudaEvent_t* ev = nullptr;
     int sm_count = 0;
     int occ[kWarpTier] = {};   // resident blocks per SM: thread kernels (0-4), wide kernels (5-8)
-    int gocc[kWarpTier] = {};  // lane-group kernels (0-4)
+    int gocc[kWarpTier] = {};  // lane-group kernels (0-4), one-warp-per-unit wide kernels (5-9)
     int mode = 0;
     int launches = 0;
     // host staging (pinned)
@@ -1086,19 +1086,25 @@ static void* tier_fn_t(int t) {
     }
 }
 
+// wide tiers: G = 8 lanes per unit for a throughput start tier (K96,
+// K128), else one warp per unit (escalations, consumers, latency mode)
 template <int MODE>
-static void* wide_fn_t(int t) {
+static void* wide_fn_t(int t, bool latency) {
     switch (t) {
-        case 5: return reinterpret_cast<void*>(wide_tier_kernel<128, MODE>);
-        case 6: return reinterpret_cast<void*>(wide_tier_kernel<256, MODE>);
-        case 7: return reinterpret_cast<void*>(wide_tier_kernel<512, MODE>);
-        default: return reinterpret_cast<void*>(wide_tier_kernel<1024, MODE>);
+        case 5: return latency ? reinterpret_cast<void*>(wide_tier_kernel<96, 32, MODE>)
+                               : reinterpret_cast<void*>(wide_tier_kernel<96, 8, MODE>);
+        case 6: return latency ? reinterpret_cast<void*>(wide_tier_kernel<128, 32, MODE>)
+                               : reinterpret_cast<void*>(wide_tier_kernel<128, 8, MODE>);
+        case 7: return reinterpret_cast<void*>(wide_tier_kernel<256, 32, MODE>);
+        case 8: return reinterpret_cast<void*>(wide_tier_kernel<512, 32, MODE>);
+        default: return reinterpret_cast<void*>(wide_tier_kernel<1024, 32, MODE>);
     }
 }
 
 // tiers 0-4: thread (or lane-group) kernels; 5-8: the wide one-warp-per-unit kernels
 static void* tier_kernel(bool group, int mode, int t) {
-    if (t >= kWideFirst) return mode == 0 ? wide_fn_t<0>(t) : mode == 1 ? wide_fn_t<1>(t) : wide_fn_t<2>(t);
+    if (t >= kWideFirst)  // `group` selects the latency form (one warp per unit)
+        return mode == 0 ? wide_fn_t<0>(t, group) : mode == 1 ? wide_fn_t<1>(t, group) : wide_fn_t<2>(t, group);
     if (group) return mode == 0 ? tier_fn_t<true, 0>(t) : mode == 1 ? tier_fn_t<true, 1>(t) : tier_fn_t<true, 2>(t);
     return mode == 0 ? tier_fn_t<false, 0>(t) : mode == 1 ? tier_fn_t<false, 1>(t) : tier_fn_t<false, 2>(t);
 }
@@ -1238,8 +1244,7 @@ static int run_plan(xb_batch* B, DevBatch& D) {
     tp.esc_to_warp = (B->flags & XB_FLAG_ESC_TO_WARP) ? 1 : 0;
     for (int t = 0; t < kWarpTier; ++t) {
         if (!D.occ[t]) CK(occupancy_blocks(false, t, mode, &D.occ[t]) ? cudaErrorUnknown : cudaSuccess);
-        if (t < kNarrowTiers && !D.gocc[t])
-            CK(occupancy_blocks(true, t, mode, &D.gocc[t]) ? cudaErrorUnknown : cudaSuccess);
+        if (!D.gocc[t]) CK(occupancy_blocks(true, t, mode, &D.gocc[t]) ? cudaErrorUnknown : cudaSuccess);
     }
     if (pn > 0) {
         // The pilot samples a stride of the units in input order (d_vals is
@@ -1307,10 +1312,12 @@ __device__ void tail_launch_tier(int t, bool group, const TierParams& P, int gri
         XB_TAIL_NARROW(3, 48)
         XB_TAIL_NARROW(4, 64)
 #undef XB_TAIL_NARROW
-        case 5: wide_tier_kernel<128, MODE><<<g, b, 0, cudaStreamTailLaunch>>>(P); break;
-        case 6: wide_tier_kernel<256, MODE><<<g, b, 0, cudaStreamTailLaunch>>>(P); break;
-        case 7: wide_tier_kernel<512, MODE><<<g, b, 0, cudaStreamTailLaunch>>>(P); break;
-        default: wide_tier_kernel<1024, MODE><<<g, b, 0, cudaStreamTailLaunch>>>(P); break;
+        // escalations on the wide tiers: one warp per unit (latency-bound)
+        case 5: wide_tier_kernel<96, 32, MODE><<<g, b, 0, cudaStreamTailLaunch>>>(P); break;
+        case 6: wide_tier_kernel<128, 32, MODE><<<g, b, 0, cudaStreamTailLaunch>>>(P); break;
+        case 7: wide_tier_kernel<256, 32, MODE><<<g, b, 0, cudaStreamTailLaunch>>>(P); break;
+        case 8: wide_tier_kernel<512, 32, MODE><<<g, b, 0, cudaStreamTailLaunch>>>(P); break;
+        default: wide_tier_kernel<1024, 32, MODE><<<g, b, 0, cudaStreamTailLaunch>>>(P); break;
     }
 }
 
@@ -1384,7 +1391,7 @@ static int run_cascade(xb_batch* B, DevBatch& D) {
     // the next tier's escalations are consumed concurrently with the start
     // tier (lane groups, when there is a wider lane-group tier); the tail
     // dispatch after the start tier finishes what is left
-    const bool concurrent = !D.all_group && !D.no_group && D.t0 + 1 < kNarrowTiers &&
+    const bool concurrent = !D.all_group && !D.no_group && D.t0 + 1 < kWarpTier &&
                             !(B->flags & (XB_FLAG_ESC_TO_WARP | XB_FLAG_SERIAL_TAIL));
     std::unique_lock<std::mutex> order;
     if (!D.all_group) {  // throughput-planned: after the previous such cascade
@@ -1398,15 +1405,12 @@ static int run_cascade(xb_batch* B, DevBatch& D) {
     if (t0 < kWarpTier) {
         // ---- the start tier ----
         tp.tier = t0;
-        if (t0 >= kWideFirst) {  // wide start: one warp per unit over the whole queue
-            tp.role = kRoleAll;
-            CK(launch_tier(false, mode, t0, tp, D.sm_count * D.occ[t0], D.stream));
-        } else if (D.all_group || D.no_group) {
+        if (D.all_group || D.no_group) {
             tp.role = kRoleAll;
             int per_sm = D.all_group ? D.gocc[t0] : D.occ[t0];
-            if (D.all_group) per_sm = std::min(per_sm, latency_blocks_per_sm(D));
+            if (D.all_group && t0 < kNarrowTiers) per_sm = std::min(per_sm, latency_blocks_per_sm(D));
             CK(launch_tier(D.all_group, mode, t0, tp, D.sm_count * per_sm, D.stream));
-        } else {  // one thread per unit, the concurrent consumer beside it
+        } else {  // throughput: one thread per unit (or 8 lanes, wide), the concurrent consumer beside it
             if (concurrent) {
                 // the next tier's list starts empty-marked
                 CK(cudaMemsetAsync(D.d_lists + int64_t(t0 + 1) * D.n_units, 0xFF, size_t(D.n_units) * 4,
@@ -1419,11 +1423,11 @@ static int run_cascade(xb_batch* B, DevBatch& D) {
             CK(launch_tier(false, mode, t0, tp,
                            std::max(1, D.sm_count * D.occ[t0] - (concurrent ? kConsumerBlocks : 0)), D.stream));
             if (concurrent) {
-                // a few high-priority lane-group blocks take the start tier's
-                // escalations while it runs.  Launched after it (API order), so
-                // tools that serialise launches run the consumer after the whole
-                // start tier: the consumer never waits on a producer that cannot
-                // run (no timeout, see group_tier_kernel)
+                // a few high-priority blocks take the start tier's escalations while
+                // it runs (lane groups, or one warp per unit on the wide tiers).
+                // Launched after it (API order), so tools that serialise launches
+                // run the consumer after the whole start tier: the consumer never
+                // waits on a producer that cannot run (no timeout)
                 CK(cudaStreamWaitEvent(D.aux_stream, D.aux_ev[0], 0));
                 TierParams cp = tp;
                 cp.tier = t0 + 1;
@@ -1444,9 +1448,9 @@ static int run_cascade(xb_batch* B, DevBatch& D) {
         plan.mode = mode;
         plan.t0 = t0;
         for (int t = t0 + 1; t < kWarpTier; ++t) {
-            if (t >= kWideFirst) {
-                plan.grid[t] = D.sm_count * std::min(D.occ[t], 2);  // few units: at most 8 warps per SM
-                plan.group[t] = 0;
+            if (t >= kWideFirst) {  // escalations: one warp per unit, at full occupancy
+                plan.grid[t] = D.sm_count * D.gocc[t];
+                plan.group[t] = 1;
             } else if (D.no_group) {
                 plan.grid[t] = D.sm_count * D.occ[t];
                 plan.group[t] = 0;

@@ -615,15 +615,14 @@ __global__ void __launch_bounds__(128) group_tier_kernel(TierParams P) {
                     volatile unsigned long long* lenp = &P.ctr->list_len[P.tier];
                     volatile unsigned long long* curp = Q.cursor;
                     for (;;) {
-                        const unsigned long long c = *curp;
-                        if (c >= *lenp) {
-                            // nothing queued: done once the start tier has finished (the
-                            // list length is final then: its last block publishes the flag
-                            // after all of its escalations)
-                            st = *(volatile int32_t*)&P.ctr->prod_finished ? 2 : 0;
-                            if (st == 2 && c < *lenp) st = 0;  // a late entry landed meanwhile
+                        // once the start tier has finished, the tail dispatch (a full
+                        // grid) takes what is still queued: stop claiming
+                        if (*(volatile int32_t*)&P.ctr->prod_finished) {
+                            st = 2;
                             break;
                         }
+                        const unsigned long long c = *curp;
+                        if (c >= *lenp) break;  // nothing queued yet
                         if (atomicCAS(Q.cursor, c, c + 1) == c) {
                             i = c;
                             const volatile uint32_t* ep = Q.q + (long long)i;

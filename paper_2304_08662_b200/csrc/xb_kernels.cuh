@@ -99,15 +99,15 @@ constexpr int kTB = 128;                // threads per block, thread tiers
 constexpr int32_t kBig = 1 << 29;       // empty live range = [kBig, -kBig]
 
 // Tiers: band widths K (slots per unit).  0-4: thread / lane-group tiers
-// (K16..K64, register bands); 5-8: wide tiers (one warp per unit, K128..
-// K1024, xb_wide.cu); 9: the generic warp tier (any band).
-constexpr int kNumTiers = 10;
+// (K16..K64, register bands); 5-9: wide tiers (G lanes per unit, K96..
+// K1024, xb_wide.cu); 10: the generic warp tier (any band).
+constexpr int kNumTiers = 11;
 constexpr int kNarrowTiers = 5;   // tiers 0..4
 constexpr int kWideFirst = 5;
-constexpr int kWarpTier = 9;
+constexpr int kWarpTier = 10;
 __host__ __device__ constexpr int tier_width(int t) {
     return t == 0 ? 16 : t == 1 ? 24 : t == 2 ? 32 : t == 3 ? 48 : t == 4 ? 64
-         : t == 5 ? 128 : t == 6 ? 256 : t == 7 ? 512 : t == 8 ? 1024 : 1 << 30;
+         : t == 5 ? 96 : t == 6 ? 128 : t == 7 ? 256 : t == 8 ? 512 : t == 9 ? 1024 : 1 << 30;
 }
 constexpr int kPilotCursor = 15;  // DevCounters::cursor slot of the pilot sample
 

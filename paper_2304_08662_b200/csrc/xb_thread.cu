@@ -746,8 +746,11 @@ __global__ void select_tier_kernel(TierParams P, int forced, int32_t* host_out) 
             best = t;
         }
     }
-    // most of the sample outgrows K64: the whole batch starts on the wide tiers
-    if (n > 0 && double(need[kNarrowTiers - 1]) > 0.5 * n) best = kWideFirst;
+    // Most of the sample outgrows K64: the whole batch starts on the wide
+    // tiers, at K128.  (A K96 start measured slower on config 4 with X = 100:
+    // 167 ms plus a 24 ms tail of the 2% of units that outgrow it, against
+    // 179 ms at K128 with no tail; K96 stays as the tier K64 escalates into.)
+    if (n > 0 && double(need[kNarrowTiers - 1]) > 0.5 * n) best = kWideFirst + 1;
     P.ctr->start_tier = best;
     *(volatile int32_t*)host_out = best;
 }

@@ -1,8 +1,9 @@
-// Wide tiers: one warp per unit, K = 128 / 256 / 512 / 1024 slots of the
-// restricted band in registers (S = K/32 consecutive slots per lane).  They
-// take the units whose live window outgrows the K64 tier -- large X, low
-// identity, the reference's default band of 1024 (pipeline.hpp:28) -- which
-// round 1 left to the generic warp tier's global-memory rows.
+// Wide tiers: G lanes per unit, K = 96 / 128 / 256 / 512 / 1024 slots of
+// the restricted band in registers (S = K/G consecutive slots per lane;
+// G = 8, 8, 16, 32, 32: four, four, two, one, one unit per warp).  They take the units whose
+// live window outgrows the K64 tier -- large X, low identity, the
+// reference's default band of 1024 (pipeline.hpp:28) -- which round 1 left
+// to the generic warp tier's global-memory rows.
 //
 // Exact reference semantics (proj/src/align.cpp:37-155), same coordinates,
 // drift-space values and window bookkeeping as the thread tier (see
@@ -18,7 +19,13 @@
 //   * the live range is two warp reductions (max of the highest live slot,
 //     min of the lowest) instead of a gathered bit mask;
 //   * a recentre shifts the rows through shared memory (rare).
-// Control flow is warp-uniform throughout: one unit per warp.
+// The groups of a warp step in lockstep (as the lane-group tiers do): the
+// main path uses full-warp shuffles segmented by G; a group whose step
+// decides its unit records the outcome and finishes the iteration as dead
+// work; the rare path and the fetch of the next unit are group-divergent and
+// use the group's mask.  (One warp per unit at K128 cost 4x the instructions
+// per cell of the K64 thread tier, measured on config 4 with X = 100:
+// per-unit bookkeeping repeated on 32 lanes.)
 #include <climits>
 #include <cstdint>
 
@@ -46,13 +53,14 @@ __device__ __forceinline__ uint32_t wlop3(uint32_t a, uint32_t b, uint32_t c) {
     return d;
 }
 
-constexpr int kWideWarps = 4;  // warps (units) per block
+constexpr int kWideWarps = 4;  // warps per block
+constexpr unsigned kFull = 0xFFFFFFFFu;
 
 }  // namespace
 
-template <int K, int MODE>
+template <int K, int G, int MODE>
 struct WState {
-    static constexpr int S = K / 32;           // slots per lane
+    static constexpr int S = K / G;            // slots per lane
     static constexpr int NW = (S + 15) / 16;   // 2-bit window words per lane (MODE 0)
     static constexpr int NB = (S + 3) / 4;     // byte window words per lane (table modes)
     static constexpr int KB = K - 1;
@@ -67,26 +75,26 @@ struct WState {
     uint32_t VWb[NB], HWb[NB];   // byte windows (table modes)
     static constexpr int RENC = MODE == 2 ? ENC_5BIT : ENC_2BIT;
     static constexpr int RPER = EncFields<RENC>::PER;
-    Reader<true, RENC> rv;       // lane 0: v symbols entering slot 0
-    Reader<false, RENC> rh;      // lane 31: h symbols entering slot K-1
+    Reader<true, RENC> rv;       // lane 0 of the group: v symbols entering slot 0
+    Reader<false, RENC> rh;      // lane G-1: h symbols entering slot K-1
 };
 
-template <int K, int MODE>
-__device__ __forceinline__ void w_limits(WState<K, MODE>& S) {
+template <int K, int G, int MODE>
+__device__ __forceinline__ void w_limits(WState<K, G, MODE>& S) {
     S.d_vm = min(2 * (S.ubase + S.n + 1), 2 * (S.m - S.ubase - K + 2) - 1);
     S.d_lim = min(S.d_vm, S.n + S.m + 2);
 }
 
 // symbol windows of this lane's slots at antidiagonal S.d, readers set up for
-// rv_r / rh_r symbols before their next refill point (lanes 0 / 31)
-template <int K, int MODE>
-__device__ __forceinline__ void w_windows(WState<K, MODE>& S, const uint32_t* __restrict__ pool, int lane,
+// rv_r / rh_r symbols before their next refill point (lanes 0 / G-1)
+template <int K, int G, int MODE>
+__device__ __forceinline__ void w_windows(WState<K, G, MODE>& S, const uint32_t* __restrict__ pool, int lane,
                                           int rv_r, int rh_r) {
-    using St = WState<K, MODE>;
+    using St = WState<K, G, MODE>;
     constexpr int SS = St::S;
     const int fd = S.d >> 1, cd = S.d - fd;
-    const int64_t a = int64_t(fd) - S.ubase - 1;  // v index of global slot 0
-    const int64_t b = int64_t(cd) + S.ubase - 1;  // h index of global slot 0
+    const int64_t a = int64_t(fd) - S.ubase - 1;  // v index of group slot 0
+    const int64_t b = int64_t(cd) + S.ubase - 1;  // h index of group slot 0
     const int k0 = lane * SS;
     if constexpr (MODE == 0) {
 #pragma unroll
@@ -115,14 +123,14 @@ __device__ __forceinline__ void w_windows(WState<K, MODE>& S, const uint32_t* __
         }
     }
     if (lane == 0) S.rv.init(pool, S.v_pos, S.vdir, a + 1, rv_r);
-    if (lane == 31) S.rh.init(pool, S.h_pos, S.hdir, b + K, rh_r);
+    if (lane == G - 1) S.rh.init(pool, S.h_pos, S.hdir, b + K, rh_r);
 }
 
 // Table modes: sentinel bytes over slots whose v or h symbol lies past the
 // view's end (see the thread tier's sentinel_windows).
-template <int K, int MODE>
-__device__ __forceinline__ void w_sentinels(WState<K, MODE>& S, int d, int k0) {
-    using St = WState<K, MODE>;
+template <int K, int G, int MODE>
+__device__ __forceinline__ void w_sentinels(WState<K, G, MODE>& S, int d, int k0) {
+    using St = WState<K, G, MODE>;
     const int fd = d >> 1, cd = d - fd;
     const int vhi = fd - S.ubase - 1 - S.n - k0;
     const int hlo = S.m - (cd + S.ubase - 1) - k0;
@@ -136,34 +144,37 @@ __device__ __forceinline__ void w_sentinels(WState<K, MODE>& S, int d, int k0) {
     }
 }
 
-// rows shifted by sh slots across the warp (new slot k = old slot k + sh,
-// vacated slots dead) through this warp's shared-memory row
-template <int SS>
-__device__ __forceinline__ void w_shift(int32_t (&R)[SS], int sh, int lane, int32_t* row) {
-    constexpr int KK = 32 * SS;
-    __syncwarp();
+// rows shifted by sh slots across the group (new slot k = old slot k + sh,
+// vacated slots dead) through the group's shared-memory row
+template <int SS, int G>
+__device__ __forceinline__ void w_shift(int32_t (&R)[SS], int sh, int lane, int32_t* row, unsigned gmask) {
+    constexpr int KK = G * SS;
+    __syncwarp(gmask);
 #pragma unroll
     for (int s = 0; s < SS; ++s) row[lane * SS + s] = R[s];
-    __syncwarp();
+    __syncwarp(gmask);
 #pragma unroll
     for (int s = 0; s < SS; ++s) {
         const int src = lane * SS + s + sh;
         R[s] = (src >= 0 && src < KK) ? row[src] : kDeadS;
     }
     XB_ASSERT(sh > -KK && sh < KK, kChkSmemRow);
-    __syncwarp();
+    __syncwarp(gmask);
 }
 
-template <int K, int MODE, bool ODD>
-__device__ __forceinline__ void wfeed(WState<K, MODE>& S, int lane) {
-    using St = WState<K, MODE>;
+// Symbols entering on d+1 (v after an odd step, h after an even one).  FM:
+// the whole warp executes the call (full-mask shuffles); else only the group.
+template <int K, int G, int MODE, bool ODD, bool FM>
+__device__ __forceinline__ void wfeed(WState<K, G, MODE>& S, int lane, unsigned gmask) {
+    using St = WState<K, G, MODE>;
     constexpr int SS = St::S;
+    const unsigned m = FM ? kFull : gmask;
     if constexpr (MODE == 0) {
         constexpr int NW = St::NW;
         constexpr int top = 2 * ((SS - 1) & 15);  // bit offset of slot SS-1 in the last word
         if constexpr (ODD) {  // v: slot k <- k-1, new symbol at slot 0 (lane 0's reader)
             const uint32_t out = (S.VW[NW - 1] >> top) & 3u;
-            uint32_t in = __shfl_up_sync(0xFFFFFFFFu, out, 1);
+            uint32_t in = __shfl_up_sync(m, out, 1, G);
             if (lane == 0) {
                 in = S.rv.cur >> 30;
                 S.rv.cur <<= 2;
@@ -171,10 +182,10 @@ __device__ __forceinline__ void wfeed(WState<K, MODE>& S, int lane) {
 #pragma unroll
             for (int w = NW - 1; w > 0; --w) S.VW[w] = __funnelshift_l(S.VW[w - 1], S.VW[w], 2);
             S.VW[0] = (S.VW[0] << 2) | in;
-        } else {  // h: slot k <- k+1, new symbol at slot K-1 (lane 31's reader)
+        } else {  // h: slot k <- k+1, new symbol at slot K-1 (lane G-1's reader)
             const uint32_t out = S.HW[0] & 3u;
-            uint32_t in = __shfl_down_sync(0xFFFFFFFFu, out, 1);
-            if (lane == 31) {
+            uint32_t in = __shfl_down_sync(m, out, 1, G);
+            if (lane == G - 1) {
                 in = S.rh.cur & 3u;
                 S.rh.cur >>= 2;
             }
@@ -188,15 +199,15 @@ __device__ __forceinline__ void wfeed(WState<K, MODE>& S, int lane) {
         constexpr int top = 8 * ((SS - 1) & 3);
         if constexpr (ODD) {
             const uint32_t out = (S.VWb[NB - 1] >> top) & 0xFFu;
-            uint32_t in = __shfl_up_sync(0xFFFFFFFFu, out, 1);
+            uint32_t in = __shfl_up_sync(m, out, 1, G);
             if (lane == 0) in = S.rv.take();
 #pragma unroll
             for (int r = NB - 1; r > 0; --r) S.VWb[r] = __funnelshift_l(S.VWb[r - 1], S.VWb[r], 8);
             S.VWb[0] = (S.VWb[0] << 8) | in;
         } else {
             const uint32_t out = S.HWb[0] & 0xFFu;
-            uint32_t in = __shfl_down_sync(0xFFFFFFFFu, out, 1);
-            if (lane == 31) in = S.rh.take();
+            uint32_t in = __shfl_down_sync(m, out, 1, G);
+            if (lane == G - 1) in = S.rh.take();
 #pragma unroll
             for (int r = 0; r < NB - 1; ++r) S.HWb[r] = __funnelshift_r(S.HWb[r], S.HWb[r + 1], 8);
             const uint32_t keep = top == 24 ? 0xFFFFFFFFu : ((1u << (top + 8)) - 1u);
@@ -212,14 +223,14 @@ struct WSink {
     bool resumable;
 };
 
-// Records the outcome of the warp's unit at the deciding step (see the
-// thread tier's finish_unit).
-template <int K, int MODE>
-__device__ __forceinline__ void wfinish(WState<K, MODE>& S, const TierParams& P, int code, int spread,
-                                        WSink& sk, int32_t beta, const int32_t (&cur)[K / 32],
-                                        const int32_t (&prv)[K / 32], int lane) {
-    constexpr int SS = K / 32;
-    constexpr int KB = WState<K, MODE>::KB;
+// Records the outcome of the group's unit at the deciding step (see the
+// thread tier's finish_unit); the rest of that iteration is dead work.
+template <int K, int G, int MODE>
+__device__ __forceinline__ void wfinish(WState<K, G, MODE>& S, const TierParams& P, int code, int spread,
+                                        WSink& sk, int32_t beta, const int32_t (&cur)[K / G],
+                                        const int32_t (&prv)[K / G], int lane, unsigned gmask) {
+    constexpr int SS = K / G;
+    constexpr int KB = WState<K, G, MODE>::KB;
     S.stop = code;
     if (code == kEscalate) {
         uint32_t entry = uint32_t(S.unit);
@@ -228,7 +239,7 @@ __device__ __forceinline__ void wfinish(WState<K, MODE>& S, const TierParams& P,
             int32_t* rec = nullptr;
             uint32_t got = 0u;
             if (lane == 0) got = alloc_record<K>(P, rec);
-            got = __shfl_sync(0xFFFFFFFFu, got, 0);
+            got = __shfl_sync(gmask, got, 0, G);
             if (got) {
                 rec = record_ptr(P.resume, got);
 #pragma unroll
@@ -254,12 +265,12 @@ __device__ __forceinline__ void wfinish(WState<K, MODE>& S, const TierParams& P,
                 entry = got;
             }
         }
-        __syncwarp();
+        __syncwarp(gmask);
         if (lane == 0) {
             __threadfence();
             const unsigned long long slot = atomicAdd(sk.esc_len, 1ull);
             XB_ASSERT(slot < P.ck_units, kChkList);
-            sk.esc_list[slot] = entry;
+            *(volatile uint32_t*)&sk.esc_list[slot] = entry;
             ++sk.esc;
         }
         return;
@@ -287,13 +298,17 @@ __device__ __forceinline__ void wfinish(WState<K, MODE>& S, const TierParams& P,
 }
 
 // One antidiagonal d.  cur holds d-2 on entry and d on exit, prv holds d-1.
-template <int K, int MODE, bool ODD>
-__device__ __forceinline__ void wstep(WState<K, MODE>& S, int32_t (&cur)[K / 32], int32_t (&prv)[K / 32],
+// FM: every group of the warp executes the step (main loop); else only this
+// group (the even step of a unit resumed at an even d, inside fetch).
+template <int K, int G, int MODE, bool ODD, bool FM>
+__device__ __forceinline__ void wstep(WState<K, G, MODE>& S, int32_t (&cur)[K / G], int32_t (&prv)[K / G],
                                       const TierParams& P, const tab_t* __restrict__ tab, int32_t gap,
-                                      int32_t X, unsigned it, int lane, WSink& sk, int32_t* srow) {
-    using St = WState<K, MODE>;
+                                      int32_t X, unsigned it, int lane, unsigned gmask, WSink& sk,
+                                      int32_t* srow) {
+    using St = WState<K, G, MODE>;
     constexpr int SS = St::S;
     constexpr int KB = St::KB;
+    const unsigned fm = FM ? kFull : gmask;
     const int d = S.d;
     const int k0 = lane * SS;
     const int32_t beta = -gap;
@@ -306,70 +321,71 @@ __device__ __forceinline__ void wstep(WState<K, MODE>& S, int32_t (&cur)[K / 32]
     [[maybe_unused]] uint32_t inv[St::NW];
 #pragma unroll
     for (int w = 0; w < St::NW; ++w) inv[w] = 0u;
-    // warp-uniform rare path
-    if (M > KB || unsigned(s_hi) > unsigned(K - 1) || unsigned(wm1) >= unsigned(P.band) || d >= S.d_lim) {
+    // group-uniform rare path (a decided unit's dead work skips it)
+    if ((M > KB || unsigned(s_hi) > unsigned(K - 1) || unsigned(wm1) >= unsigned(P.band) || d >= S.d_lim) &&
+        !S.stop) {
         const bool e1 = S.hs1 < 0, e2 = S.hs2 < 0;
         if ((e1 && e2) || d > S.n + S.m + 1) {
-            wfinish<K, MODE>(S, P, kDone, 0, sk, beta, cur, prv, lane);
-            return;
-        }
-        int lo = kBig, hi = -kBig;
-        if (!e1) {
-            lo = KB - S.lr1 - (ODD ? 1 : 0);
-            hi = S.hs1 + (ODD ? 0 : 1);
-        }
-        if (!e2) {
-            lo = min(lo, KB - S.lr2);
-            hi = max(hi, S.hs2);
-        }
-        const int fd = d >> 1;
-        int A = fd - S.ubase;
-        const int w = min(hi, A - max(d - S.m, 0)) - max(lo, A - min(d, S.n)) + 1;
-        if (w > P.band) {
-            wfinish<K, MODE>(S, P, kBand, w, sk, beta, cur, prv, lane);
-            return;
-        }
-        if (lo < 0 || hi > K - 1) {
-            const int wu = hi - lo + 1;
-            if (wu > K) {
-                wfinish<K, MODE>(S, P, kEscalate, 0, sk, beta, cur, prv, lane);
-                return;
-            }
-            const int sh = lo - ((K - wu) >> 1);  // new slot 0 = old slot sh
-            w_shift<SS>(cur, sh, lane, srow);
-            w_shift<SS>(prv, sh, lane, srow);
-            S.ubase += sh;
+            wfinish<K, G, MODE>(S, P, kDone, 0, sk, beta, cur, prv, lane, gmask);  // align.cpp:61-66
+        } else {
+            int lo = kBig, hi = -kBig;
             if (!e1) {
-                S.hs1 -= sh;
-                S.lr1 += sh;
+                lo = KB - S.lr1 - (ODD ? 1 : 0);
+                hi = S.hs1 + (ODD ? 0 : 1);
             }
             if (!e2) {
-                S.hs2 -= sh;
-                S.lr2 += sh;
+                lo = min(lo, KB - S.lr2);
+                hi = max(hi, S.hs2);
             }
-            A -= sh;
-            w_limits(S);
-            constexpr int PER = St::RPER;
-            const int to_refill = PER - int(it & (PER - 1));
-            w_windows(S, P.pool, lane, ODD ? to_refill : to_refill - 1, to_refill);
-        }
-        if (d >= S.d_vm) {
-            // slots inside the matrix: i <= n  <=>  k >= klo ;  j <= m  <=>  k <= khi
-            const int klo = A - S.n;
-            const int khi = S.m - (d - fd) - S.ubase;
-            const int l = max(klo - k0, 0), h = min(min(khi, K - 1) - k0, SS - 1);
-            vml = wbits(l, h);
-            if constexpr (MODE == 0) {
-#pragma unroll
-                for (int ww = 0; ww < St::NW; ++ww) {
-                    const int lw = max(l - 16 * ww, 0), hw = min(h - 16 * ww, 15);
-                    inv[ww] = ~((lw > hw) ? 0u : wbits(2 * lw, 2 * hw + 1));
-                }
+            const int fd = d >> 1;
+            int A = fd - S.ubase;
+            const int w = min(hi, A - max(d - S.m, 0)) - max(lo, A - min(d, S.n)) + 1;
+            if (w > P.band) {  // align.cpp:93-94
+                wfinish<K, G, MODE>(S, P, kBand, w, sk, beta, cur, prv, lane, gmask);
             } else {
-                w_sentinels(S, d, k0);
+                if (lo < 0 || hi > K - 1) {
+                    const int wu = hi - lo + 1;
+                    if (wu > K) {
+                        wfinish<K, G, MODE>(S, P, kEscalate, 0, sk, beta, cur, prv, lane, gmask);
+                    } else {
+                        const int sh = lo - ((K - wu) >> 1);  // new slot 0 = old slot sh
+                        w_shift<SS, G>(cur, sh, lane, srow, gmask);
+                        w_shift<SS, G>(prv, sh, lane, srow, gmask);
+                        S.ubase += sh;
+                        if (!e1) {
+                            S.hs1 -= sh;
+                            S.lr1 += sh;
+                        }
+                        if (!e2) {
+                            S.hs2 -= sh;
+                            S.lr2 += sh;
+                        }
+                        A -= sh;
+                        w_limits(S);
+                        constexpr int PER = St::RPER;
+                        const int to_refill = PER - int(it & (PER - 1));
+                        w_windows(S, P.pool, lane, ODD ? to_refill : to_refill - 1, to_refill);
+                    }
+                }
+                if (!S.stop && d >= S.d_vm) {
+                    // slots inside the matrix: i <= n  <=>  k >= klo ;  j <= m  <=>  k <= khi
+                    const int klo = A - S.n;
+                    const int khi = S.m - (d - fd) - S.ubase;
+                    const int l = max(klo - k0, 0), h = min(min(khi, K - 1) - k0, SS - 1);
+                    vml = wbits(l, h);
+                    if constexpr (MODE == 0) {
+#pragma unroll
+                        for (int ww = 0; ww < St::NW; ++ww) {
+                            const int lw = max(l - 16 * ww, 0), hw = min(h - 16 * ww, 15);
+                            inv[ww] = ~((lw > hw) ? 0u : wbits(2 * lw, 2 * hw + 1));
+                        }
+                    } else {
+                        w_sentinels(S, d, k0);
+                    }
+                }
+                wm1 = max(w, 0) - 1;  // a clamped-empty row counts no cells (align.cpp:84-90)
             }
         }
-        wm1 = max(w, 0) - 1;  // a clamped-empty row counts no cells (align.cpp:84-90)
     }
     S.cells += wm1 + 1;
     S.delta_w = max(S.delta_w, wm1 + 1);
@@ -377,10 +393,10 @@ __device__ __forceinline__ void wstep(WState<K, MODE>& S, int32_t (&cur)[K / 32]
     // gap source across the lane edge
     int32_t edge;
     if constexpr (ODD) {
-        edge = __shfl_down_sync(0xFFFFFFFFu, prv[0], 1);
-        if (lane == 31) edge = kDeadS;
+        edge = __shfl_down_sync(fm, prv[0], 1, G);
+        if (lane == G - 1) edge = kDeadS;
     } else {
-        edge = __shfl_up_sync(0xFFFFFFFFu, prv[SS - 1], 1);
+        edge = __shfl_up_sync(fm, prv[SS - 1], 1, G);
         if (lane == 0) edge = kDeadS;
     }
     // match bytes (see the thread tier): byte j of Z[w][q] = 1 + 2*match of slot 16w + 4j + q
@@ -394,9 +410,8 @@ __device__ __forceinline__ void wstep(WState<K, MODE>& S, int32_t (&cur)[K / 32]
             for (int q = 0; q < 4; ++q) Z[ww][q] = ((z >> (2 * q)) & 0x02020202u) | 0x01010101u;
         }
     }
-    // pass 1: candidates; lane maximum and its highest slot (key = 64 cand + s)
+    // pass 1: candidates and the lane maximum
     int32_t cand[SS];
-    int32_t mk = -(1 << 30);
 #pragma unroll
     for (int s = SS - 1; s >= 0; --s) {
         const int32_t dg = cur[s];
@@ -423,76 +438,112 @@ __device__ __forceinline__ void wstep(WState<K, MODE>& S, int32_t (&cur)[K / 32]
             un = prv[s];
         }
         cand[s] = __vimax3_s32(db, ln, un);
-        mk = max(mk, cand[s] * 64 + s);
     }
-    const int32_t mv = mk >> 6;  // lane maximum (drift space)
-    // suffix maximum over the lanes (ascending i = descending lane)
+    // lane maximum with its highest slot: keys 64 cand + s (IMAD on the FMA
+    // pipe; the ALU pipe carries the recurrence, chain and compares)
+    int32_t mk = -(1 << 30);
+#pragma unroll
+    for (int s = SS - 1; s >= 0; s -= 2) {
+        int32_t k1, k2;
+        asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(k1) : "r"(cand[s]), "r"(P.r64), "r"(s));
+        if (s >= 1) {
+            asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(k2) : "r"(cand[s >= 1 ? s - 1 : 0]), "r"(P.r64), "r"(s - 1));
+            mk = __vimax3_s32(mk, k1, k2);
+        } else {
+            mk = max(mk, k1);
+        }
+    }
+    const int32_t mv = mk >> 6;
+    // suffix maximum over the group's lanes (ascending i = descending lane)
     int32_t incl = mv;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int32_t y = __shfl_down_sync(0xFFFFFFFFu, incl, o);
-        if (lane + o < 32) incl = max(incl, y);
+    for (int o = 1; o < G; o <<= 1) {
+        const int32_t y = __shfl_down_sync(fm, incl, o, G);
+        if (lane + o < G) incl = max(incl, y);
     }
-    int32_t above = __shfl_down_sync(0xFFFFFFFFu, incl, 1);
-    if (lane == 31) above = -(1 << 30);
-    const int32_t gmax = __shfl_sync(0xFFFFFFFFu, incl, 0);
+    int32_t above = __shfl_down_sync(fm, incl, 1, G);
+    if (lane == G - 1) above = -(1 << 30);
+    const int32_t gmax = __shfl_sync(fm, incl, 0, G);
     // pass 2: the lane's chain (align.cpp:122-129: prune against the running
     // best, which includes the cell itself), drop test, live bits
     int32_t c = max(S.Tv, above - X);
     uint32_t dm = 0u;
+    int32_t kept[SS];  // the row after the drop test
 #pragma unroll
     for (int s = SS - 1; s >= 0; --s) {
         c = __viaddmax_s32(cand[s], -X, c);
-        if (cand[s] < c) {
-            cand[s] = kDeadS;
-            dm |= 1u << s;
-        }
-        cur[s] = cand[s];
+        // kill and dead bit as predicated IMADs with opaque constants (FMA
+        // pipe; the ALU pipe carries the max / compare chain), as in the
+        // thread tier's slot_tail
+        kept[s] = cand[s];
+        asm("{\n\t.reg .pred p;\n\t"
+            "setp.lt.s32 p, %2, %3;\n\t"
+            "@p mad.lo.s32 %0, %0, %4, %6;\n\t"
+            "@p mad.lo.u32 %1, %5, %7, %1;\n\t}"
+            : "+r"(kept[s]), "+r"(dm)
+            : "r"(cand[s]), "r"(c), "r"(P.zero), "r"(P.one), "n"(kDeadS), "r"(1u << (s & 31)));
     }
-    // running best (align.cpp:123-127): strict improvement, first cell wins
+    // running best (align.cpp:123-127): strict improvement, first cell wins:
+    // the highest lane holding the maximum, its highest slot holding it
+    // (group-uniform branch: both reductions on the group's mask)
     if (gmax - X > S.Tv) {
+        const unsigned bal = __ballot_sync(gmask, mv == gmax);
+        const int bl = 31 - __clz(bal) - (threadIdx.x & 31 & ~(G - 1));
+        const int bs = __shfl_sync(gmask, mk & 63, bl, G);
         S.Tv = gmax - X;
         S.best_d = d;
-        const unsigned bal = __ballot_sync(0xFFFFFFFFu, mv == gmax);
-        const int bl = 31 - __clz(bal);
-        const int bs = __shfl_sync(0xFFFFFFFFu, mk & 63, bl);
         S.best_u = S.ubase + bl * SS + bs;
     }
-    // live slots of row d (align.cpp:138-145)
+#pragma unroll
+    for (int s = 0; s < SS; ++s) cur[s] = kept[s];
+    // live slots of row d (align.cpp:138-145): two group reductions
     S.hs2 = S.hs1;
     S.lr2 = S.lr1;
     {
         const uint32_t lv = ~dm & vml;
         const int hs_l = lv ? k0 + wbfind(lv) : -1;
         const int ls_l = lv ? k0 + __ffs(lv) - 1 : kBig;
-        const int hs = __reduce_max_sync(0xFFFFFFFFu, hs_l);
-        const int ls = __reduce_min_sync(0xFFFFFFFFu, ls_l);
+        const int hs = __reduce_max_sync(gmask, hs_l);
+        const int ls = __reduce_min_sync(gmask, ls_l);
         S.hs1 = hs;
         S.lr1 = hs < 0 ? -1 : KB - ls;
     }
-    wfeed<K, MODE, ODD>(S, lane);
+    wfeed<K, G, MODE, ODD, FM>(S, lane, gmask);
     S.d = d + 1;
 }
 
-// resident blocks per SM the register budget is sized for
-template <int K>
+// Resident blocks per SM the register budget is sized for: 128 registers
+// at 4 blocks while S <= 16 (the 2-bit table mode needs ~160: 3 blocks).
+template <int K, int G, int MODE>
 constexpr int wide_min_blocks() {
-    return K <= 128 ? 6 : K <= 256 ? 4 : K <= 512 ? 2 : 1;
+    return K / G > 16 ? 1 : MODE == 1 ? 3 : 4;
 }
 
-template <int K, int MODE>
-__global__ void __launch_bounds__(32 * kWideWarps, wide_min_blocks<K>()) wide_tier_kernel(TierParams P) {
-    using St = WState<K, MODE>;
+// G lanes per unit.  G = 8 (four units per warp) is the throughput form,
+// for a wide start tier over a whole batch; G = 32 (one unit per warp, the
+// shortest step) serves escalations, which are few and latency-bound.
+// kRoleConsumer (G = 32): takes the escalations of a wide start tier while
+// it runs, with the lane-group consumer's protocol (xb_group.cu): claim a
+// published slot, wait for its entry, leave once the start tier has
+// finished and the list is drained; the tail dispatch takes what is left.
+template <int K, int G, int MODE>
+__global__ void __launch_bounds__(32 * kWideWarps, wide_min_blocks<K, G, MODE>()) wide_tier_kernel(TierParams P) {
+    using St = WState<K, G, MODE>;
     constexpr int SS = St::S;
     constexpr int KB = St::KB;
+    constexpr int PER = St::RPER;
     __shared__ tab_t tab[MODE == 0 ? 1 : kTabWords];
-    __shared__ int32_t rows[kWideWarps][K];  // recentring scratch, one row per warp
+    __shared__ int32_t rows[kWideWarps * 32 / G][K];  // recentring scratch, one row per group
     const int32_t gap = P.scheme->gap, X = P.scheme->x;
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
+    const int wl = threadIdx.x & 31;
+    const int lane = wl % G;
+    const int gbase = wl - lane;
+    const unsigned gmask = (G == 32 ? kFull : ((1u << G) - 1u)) << gbase;
+    int32_t* srow = rows[threadIdx.x / G];
     const int k0 = lane * SS;
     Queue Q;
-    if (P.pilot || P.role == kRoleConsumer || !make_queue(P, Q) || Q.len == 0) return;
+    const bool consumer = P.role == kRoleConsumer;
+    if (P.pilot || !make_queue(P, Q) || (!consumer && Q.len == 0)) return;
     if constexpr (MODE != 0) {
         tab_fill(tab, P.scheme, gap);
         __syncthreads();
@@ -504,122 +555,206 @@ __global__ void __launch_bounds__(32 * kWideWarps, wide_min_blocks<K>()) wide_ti
     sk.units = sk.cells = sk.esc = 0;
     sk.resumable = next_tier != kWarpTier;
 
+    // Every group of the warp executes every step; a group without a unit
+    // steps on harmless state with stop set (no rare path, no output, no
+    // loads: its reader refills are skipped, its windows hold valid codes).
     St S;
+    S.m = S.n = 0;
+    S.stop = kDone;
+    S.rv.cur = S.rh.cur = 0u;
+    S.rv.w0 = S.rv.w1 = S.rh.w0 = S.rh.w1 = 0u;
+    S.rv.sh = S.rh.sh = 0u;
+#pragma unroll
+    for (int w = 0; w < St::NW; ++w) S.VW[w] = S.HW[w] = 0u;
+#pragma unroll
+    for (int r = 0; r < St::NB; ++r) S.VWb[r] = S.HWb[r] = 0u;
+    S.hs1 = S.hs2 = S.lr1 = S.lr2 = -1;
+    S.Tv = 0;
+    S.d = 1;
+    S.ubase = 0;
+    S.d_vm = S.d_lim = 1 << 30;
     int32_t E[SS], O[SS];
-    for (;;) {
-        // ---- next unit (warp-uniform) ----
-        unsigned long long i = Q.len;
-        // a plain read first: warps arriving after the queue ran dry leave
-        // without queueing on the cursor's atomic
-        if (lane == 0 && *(volatile unsigned long long*)Q.cursor < Q.len) i = atomicAdd(Q.cursor, 1ull);
-        i = __shfl_sync(0xFFFFFFFFu, i, 0);
-        if (i >= Q.len) break;
-        XB_ASSERT(i * Q.stride < P.ck_units, kChkList);
-        const uint32_t e = Q.q[(long long)i * Q.stride];
-        uint32_t unit = e;
-        const int32_t* rec = nullptr;
-        if (e & kResumeFlag) {
-            rec = record_ptr(P.resume, e);
-            unit = uint32_t(__ldcg(rec + kRecUnit));
-        }
-        XB_ASSERT(unit < P.ck_units, kChkUnit);
-        const DevUnit u = P.units[unit];
-        if (u.route != 0) continue;  // guard failed: the warp tier's (prep listed it there)
-        S.unit = int32_t(unit);
-        S.h_pos = u.h_pos;
-        S.v_pos = u.v_pos;
-        S.m = u.h_len;
-        S.n = u.v_len;
-        S.hdir = u.dir & 1;
-        S.vdir = (u.dir >> 1) & 1;
-        S.stop = 0;
-        // per-unit refill schedule (the warp holds one unit): refills at the
-        // start of iterations PER, 2 PER, ...; each iteration consumes one v and
-        // one h symbol, so a fresh reader covers the PER symbols before the first
-        unsigned it = 0;
-        constexpr int PER = St::RPER;
-        if (!rec) {
-            S.d = 1;
-            S.ubase = -(K / 2);
-            S.hs1 = K / 2;
-            S.lr1 = KB - K / 2;
-            S.hs2 = S.lr2 = -1;
-            S.Tv = 1;  // T + beta d + 1 at d = 0, T = 0
-            S.best_d = S.best_u = 0;
-            S.delta_w = 1;
-            S.cells = 1;
 #pragma unroll
-            for (int s = 0; s < SS; ++s) {
-                O[s] = kDeadS;
-                E[s] = (k0 + s == K / 2) ? X + 1 : kDeadS;  // s(0,0) = 0 + 0 + off
+    for (int s = 0; s < SS; ++s) E[s] = O[s] = kDeadS;
+    bool active = false;
+    bool waiting = consumer;  // a consumer group with no unit, still looking for one
+    unsigned it = 0xFFFFFFFFu;  // warp-uniform iteration counter (two antidiagonals each)
+    // the group's next unit; runs at the end of iteration `it` (group-divergent)
+    auto fetch = [&]() __attribute__((always_inline)) {
+        active = false;
+        for (;;) {
+            unsigned long long i = Q.len;
+            uint32_t e = 0;
+            if (consumer) {
+                int st = 0;  // 0 nothing queued yet, 1 claimed slot i (entry e), 2 done
+                if (lane == 0) {
+                    volatile unsigned long long* lenp = &P.ctr->list_len[P.tier];
+                    volatile unsigned long long* curp = Q.cursor;
+                    for (;;) {
+                        // once the start tier has finished, the tail dispatch (a full
+                        // grid) takes what is still queued: stop claiming
+                        if (*(volatile int32_t*)&P.ctr->prod_finished) {
+                            st = 2;
+                            break;
+                        }
+                        const unsigned long long c = *curp;
+                        if (c >= *lenp) break;  // nothing queued yet
+                        if (atomicCAS(Q.cursor, c, c + 1) == c) {
+                            i = c;
+                            const volatile uint32_t* ep = Q.q + (long long)i;
+                            while ((e = *ep) == kEmptyEntry) __nanosleep(64);
+                            __threadfence();  // the entry's resume record is visible past this point
+                            st = 1;
+                            break;
+                        }
+                    }
+                }
+                st = __shfl_sync(gmask, st, 0, G);
+                if (st != 1) {
+                    waiting = st == 0;
+                    S.stop = kDone;
+                    S.m = S.n = 0;
+                    return;
+                }
+                i = __shfl_sync(gmask, i, 0, G);
+                e = __shfl_sync(gmask, e, 0, G);
+            } else {
+                // a plain read first: groups arriving after the queue ran dry leave
+                // without queueing on the cursor's atomic
+                if (lane == 0 && *(volatile unsigned long long*)Q.cursor < Q.len) i = atomicAdd(Q.cursor, 1ull);
+                i = __shfl_sync(gmask, i, 0, G);
+                if (i >= Q.len) {
+                    S.stop = kDone;
+                    S.m = S.n = 0;
+                    return;
+                }
+                XB_ASSERT(i * Q.stride < P.ck_units, kChkList);
+                e = Q.q[(long long)i * Q.stride];
             }
-            w_limits(S);
-            w_windows(S, P.pool, lane, PER, PER);
-        } else {
-            // continue from a narrower tier's record, centred (see resume_unit)
-            const int ko = __ldcg(rec + kRecK);
-            const int off = (K - ko) >> 1;
-            const int d = __ldcg(rec + kRecD);
-            S.ubase = __ldcg(rec + kRecUbase) - off;
-            S.Tv = __ldcg(rec + kRecTc) >> 6;
-            S.best_d = __ldcg(rec + kRecBestD);
-            S.best_u = __ldcg(rec + kRecBestU);
-            S.cells = __ldcg(rec + kRecCells);
-            S.delta_w = __ldcg(rec + kRecDeltaW);
-            const int h1 = __ldcg(rec + kRecHs1), l1 = __ldcg(rec + kRecLs1);
-            const int h2 = __ldcg(rec + kRecHs2), l2 = __ldcg(rec + kRecLs2);
-            S.hs1 = h1 < 0 ? -1 : h1 + off;
-            S.lr1 = h1 < 0 ? -1 : KB - (l1 + off);
-            S.hs2 = h2 < 0 ? -1 : h2 + off;
-            S.lr2 = h2 < 0 ? -1 : KB - (l2 + off);
-            const bool odd = d & 1;
+            uint32_t unit = e;
+            const int32_t* rec = nullptr;
+            if (e & kResumeFlag) {
+                rec = record_ptr(P.resume, e);
+                unit = uint32_t(__ldcg(rec + kRecUnit));
+            }
+            XB_ASSERT(unit < P.ck_units, kChkUnit);
+            const DevUnit u = P.units[unit];
+            if (u.route != 0) continue;  // guard failed: the warp tier's (prep listed it there)
+            S.unit = int32_t(unit);
+            S.h_pos = u.h_pos;
+            S.v_pos = u.v_pos;
+            S.m = u.h_len;
+            S.n = u.v_len;
+            S.hdir = u.dir & 1;
+            S.vdir = (u.dir >> 1) & 1;
+            S.stop = 0;
+            const int r = (PER - 1) - int(it & (PER - 1));  // symbols before the next refill point
+            if (!rec) {
+                S.d = 1;
+                S.ubase = -(K / 2);
+                S.hs1 = K / 2;
+                S.lr1 = KB - K / 2;
+                S.hs2 = S.lr2 = -1;
+                S.Tv = 1;  // T + beta d + 1 at d = 0, T = 0
+                S.best_d = S.best_u = 0;
+                S.delta_w = 1;
+                S.cells = 1;
 #pragma unroll
-            for (int s = 0; s < SS; ++s) {
-                const int src = k0 + s - off;
-                const bool in = src >= 0 && src < ko;
-                const int32_t vc = in ? __ldcg(rec + kRecRows + src) : kDeadS;       // row d-2
-                const int32_t vp = in ? __ldcg(rec + kRecRows + ko + src) : kDeadS;  // row d-1
-                O[s] = odd ? vc : vp;
-                E[s] = odd ? vp : vc;
+                for (int s = 0; s < SS; ++s) {
+                    O[s] = kDeadS;
+                    E[s] = (k0 + s == K / 2) ? X + 1 : kDeadS;  // s(0,0) = 0 + 0 + off
+                }
+                w_limits(S);
+                w_windows(S, P.pool, lane, r, r);
+            } else {
+                // continue from a narrower tier's record, centred (see resume_unit)
+                const int ko = __ldcg(rec + kRecK);
+                const int off = (K - ko) >> 1;
+                const int d = __ldcg(rec + kRecD);
+                S.ubase = __ldcg(rec + kRecUbase) - off;
+                S.Tv = __ldcg(rec + kRecTc) >> 6;
+                S.best_d = __ldcg(rec + kRecBestD);
+                S.best_u = __ldcg(rec + kRecBestU);
+                S.cells = __ldcg(rec + kRecCells);
+                S.delta_w = __ldcg(rec + kRecDeltaW);
+                const int h1 = __ldcg(rec + kRecHs1), l1 = __ldcg(rec + kRecLs1);
+                const int h2 = __ldcg(rec + kRecHs2), l2 = __ldcg(rec + kRecLs2);
+                S.hs1 = h1 < 0 ? -1 : h1 + off;
+                S.lr1 = h1 < 0 ? -1 : KB - (l1 + off);
+                S.hs2 = h2 < 0 ? -1 : h2 + off;
+                S.lr2 = h2 < 0 ? -1 : KB - (l2 + off);
+                const bool odd = d & 1;
+#pragma unroll
+                for (int s = 0; s < SS; ++s) {
+                    const int src = k0 + s - off;
+                    const bool in = src >= 0 && src < ko;
+                    const int32_t vc = in ? __ldcg(rec + kRecRows + src) : kDeadS;       // row d-2
+                    const int32_t vp = in ? __ldcg(rec + kRecRows + ko + src) : kDeadS;  // row d-1
+                    O[s] = odd ? vc : vp;
+                    E[s] = odd ? vp : vc;
+                }
+                // the loop steps odd then even antidiagonals; a record at an even d
+                // runs its even step here (readers set up with a full refill period:
+                // this happens before the next refill point), and the group joins
+                // the loop at an odd d
+                S.d = odd ? d : d - 1;
+                w_windows(S, P.pool, lane, odd ? r : PER - 1, odd ? r : PER - 1);
+                S.d = d;
+                w_limits(S);
+                if (!odd) {
+                    wfeed<K, G, MODE, true, false>(S, lane, gmask);
+                    wstep<K, G, MODE, false, false>(S, E, O, P, tab, gap, X, it, lane, gmask, sk, srow);
+                    if (!S.stop) w_windows(S, P.pool, lane, r, r);  // the loop's refill schedule
+                }
             }
-            // the loop steps odd then even antidiagonals; a record at an even d
-            // runs its even step first, with the windows built at d-1 and fed v
-            S.d = odd ? d : d - 1;
-            w_windows(S, P.pool, lane, PER, PER);
-            S.d = d;
-            w_limits(S);
-            if (!odd) {
-                wfeed<K, MODE, true>(S, lane);
-                wstep<K, MODE, false>(S, E, O, P, tab, gap, X, it, lane, sk, rows[warp]);
-                if (!S.stop) w_windows(S, P.pool, lane, PER, PER);
-            }
+            active = true;
+            return;
         }
-        // ---- the unit's antidiagonals, odd then even ----
-        while (!S.stop) {
-            if ((it & (PER - 1)) == 0 && it) {
-                if (lane == 0) S.rv.refill(P.pool);
-                if (lane == 31) S.rh.refill(P.pool);
-            }
-            wstep<K, MODE, true>(S, O, E, P, tab, gap, X, it, lane, sk, rows[warp]);
-            if (S.stop) break;
-            wstep<K, MODE, false>(S, E, O, P, tab, gap, X, it, lane, sk, rows[warp]);
+    };
+    fetch();
+    it = 0;
+    while (__any_sync(kFull, active || waiting)) {
+        if (consumer && !__any_sync(kFull, active)) {  // nothing queued for this warp yet
+            __nanosleep(2000);
+            if (waiting) fetch();
             ++it;
+            continue;
+        }
+        if (active && (it & (PER - 1)) == 0) {  // the same iteration for every group
+            if (lane == 0) S.rv.refill(P.pool);
+            if (lane == G - 1) S.rh.refill(P.pool);
+        }
+        wstep<K, G, MODE, true, true>(S, O, E, P, tab, gap, X, it, lane, gmask, sk, srow);
+        wstep<K, G, MODE, false, true>(S, E, O, P, tab, gap, X, it, lane, gmask, sk, srow);
+        // outcome recorded by the deciding step; idle consumer groups poll every 8th iteration
+        if ((active && S.stop) || (consumer && !active && waiting && (it & 7) == 0)) fetch();
+        ++it;
+    }
+    if (lane == 0) {
+        if (sk.units) atomicAdd(&P.ctr->units[P.tier], sk.units);
+        if (sk.cells) atomicAdd(&P.ctr->cells[P.tier], sk.cells);
+        if (sk.esc) atomicAdd(&P.ctr->escalated[P.tier], sk.esc);
+    }
+    if (P.role == kRoleStart) {  // tell a concurrent escalation consumer when the last block is done
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            if (atomicAdd(&P.ctr->prod_done, 1u) == gridDim.x - 1) atomicExch(&P.ctr->prod_finished, 1);
         }
     }
-    if (lane != 0) return;
-    if (sk.units) atomicAdd(&P.ctr->units[P.tier], sk.units);
-    if (sk.cells) atomicAdd(&P.ctr->cells[P.tier], sk.cells);
-    if (sk.esc) atomicAdd(&P.ctr->escalated[P.tier], sk.esc);
 }
 
-#define XB_WINST(K)                                                 \
-    template __global__ void wide_tier_kernel<K, 0>(TierParams);    \
-    template __global__ void wide_tier_kernel<K, 1>(TierParams);    \
-    template __global__ void wide_tier_kernel<K, 2>(TierParams);
-XB_WINST(128)
-XB_WINST(256)
-XB_WINST(512)
-XB_WINST(1024)
+#define XB_WINST(K, G)                                                 \
+    template __global__ void wide_tier_kernel<K, G, 0>(TierParams);    \
+    template __global__ void wide_tier_kernel<K, G, 1>(TierParams);    \
+    template __global__ void wide_tier_kernel<K, G, 2>(TierParams);
+XB_WINST(96, 8)
+XB_WINST(128, 8)
+XB_WINST(96, 32)
+XB_WINST(128, 32)
+XB_WINST(256, 32)
+XB_WINST(512, 32)
+XB_WINST(1024, 32)
 #undef XB_WINST
 
 }  // namespace xb

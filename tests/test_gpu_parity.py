@@ -57,13 +57,14 @@ def _by_scheme(entries):
 # 64 = NO_GROUP (one thread per unit), 32 = GROUP (lane groups throughout),
 # 8 | t << 8 = start at tier t without the pilot
 # 128 = THROUGHPUT (pilot + cost model even for a small batch)
-# 8 | t << 8 with t = 5..8: start on the wide tiers (one warp per unit, K128..K1024)
+# 8 | t << 8 with t = WIDE_FIRST..: start on the wide tiers (8-32 lanes per unit, K96..K1024)
+from paper_2304_08662_b200.capi import NUM_TIERS, TIER_WIDTHS, WARP_TIER, WIDE_FIRST  # noqa: E402
 TIER_FLAGS = ([0, 2, 128, 128 | 64] + [64 | 8 | (t << 8) for t in range(5)]
-              + [32 | 8 | (t << 8) for t in range(5)] + [8 | (t << 8) for t in range(5, 9)])
+              + [32 | 8 | (t << 8) for t in range(5)] + [8 | (t << 8) for t in range(WIDE_FIRST, WARP_TIER)])
 TIER_IDS = (["auto", "warp_tier_only", "pilot_cascade", "thread_pilot_cascade"]
             + [f"thread_k{w}" for w in (16, 24, 32, 48, 64)]
             + [f"group_k{w}" for w in (16, 24, 32, 48, 64)]
-            + [f"wide_k{w}" for w in (128, 256, 512, 1024)])
+            + [f"wide_k{w}" for w in TIER_WIDTHS[WIDE_FIRST:]])
 
 
 @pytest.mark.parametrize("flags", TIER_FLAGS, ids=TIER_IDS)
@@ -367,7 +368,7 @@ def test_route_guard_mixed_batch(xb, oracle):
     pool = xb.DevicePool(xb.ScoringScheme.match_mismatch(1, -2, -2, 10), sym, np.array(off))
     out = xb.extend_units(pool, units, band)
     st = xb.xband.last_stats()
-    assert st["units_tier"][9] == 2 and sum(st["units_tier"][:9]) == 3, st["units_tier"]
+    assert st["units_tier"][WARP_TIER] == 2 and sum(st["units_tier"][:WARP_TIER]) == 3, st["units_tier"]
     assert sum(st["escalated"]) == 0, st["escalated"]
     so = oracle.scheme_mm(1, -2, -2, 10)
     for q, (h, v) in enumerate(entries):
@@ -557,8 +558,10 @@ WIDE_CASES = {
 
 
 @pytest.mark.parametrize("case", sorted(WIDE_CASES))
-@pytest.mark.parametrize("flags", [0, 128, 32, 64 | 8, 8 | (5 << 8), 8 | (8 << 8), 16],
-                         ids=["auto", "pilot", "groups", "thread_k16", "wide_k128", "wide_k1024", "esc_to_warp"])
+@pytest.mark.parametrize("flags", [0, 128, 32, 64 | 8, 8 | (WIDE_FIRST << 8), 8 | ((WIDE_FIRST + 1) << 8),
+                                   8 | ((WARP_TIER - 1) << 8), 16],
+                         ids=["auto", "pilot", "groups", "thread_k16", "wide_k96", "wide_k128", "wide_k1024",
+                              "esc_to_warp"])
 def test_wide_tiers_vs_oracle(xb, oracle, case, flags):
     from paper_2304_08662_b200 import synth
     cfg, scale, x, band, kind = WIDE_CASES[case]
@@ -578,9 +581,9 @@ def test_wide_tiers_vs_oracle(xb, oracle, case, flags):
     eq = result_rows_equal(out, exp)
     assert eq.all(), f"{(~eq).sum()} of {len(eq)} sides differ; first {np.nonzero(~eq)[0][:5]}"
     assert (ss == ess).all()
-    wide_units = sum(st["units_tier"][5:9])
-    if flags in (8 | (5 << 8), 8 | (8 << 8)):  # wide start: every thread-tier-routable unit is wide
-        assert sum(st["units_tier"][:5]) == 0 and wide_units > 0, st["units_tier"]
+    wide_units = sum(st["units_tier"][WIDE_FIRST:WARP_TIER])
+    if flags & 8 and flags >> 8 >= WIDE_FIRST:  # wide start: every thread-tier-routable unit is wide
+        assert sum(st["units_tier"][:WIDE_FIRST]) == 0 and wide_units > 0, st["units_tier"]
     elif flags != 16 and (exp["delta_w"] > 66).any():  # windows beyond K64 (+ slack) reach the wide tiers
         assert wide_units > 0, st["units_tier"]
     if case == "c4_x300_band200":
@@ -597,7 +600,7 @@ def test_wide_tier_is_the_start_for_wide_batches(xb):
     xb.extend_tasks(pool, ds.tasks, ds.k, 1024, exec_flags=128)
     st = xb.xband.last_stats()
     assert st["start_tier"] >= 5, st
-    assert sum(st["units_tier"][:5]) == 0 and sum(st["units_tier"][5:9]) > 0, st["units_tier"]
+    assert sum(st["units_tier"][:WIDE_FIRST]) == 0 and sum(st["units_tier"][WIDE_FIRST:WARP_TIER]) > 0, st["units_tier"]
 
 
 def test_locality_shards_same_results(xb):
