@@ -56,6 +56,24 @@ __device__ __forceinline__ uint32_t wlop3(uint32_t a, uint32_t b, uint32_t c) {
 constexpr int kWideWarps = 4;  // warps per block
 constexpr unsigned kFull = 0xFFFFFFFFu;
 
+// Maximum / minimum over the G lanes of a group.  One warp per unit: REDUX.
+// Smaller groups: butterfly shuffles on the segment (a REDUX on a partial
+// mask compiles to a collective loop with divergent branches).
+template <int G>
+__device__ __forceinline__ int group_max(int v, unsigned m) {
+    if constexpr (G == 32) return __reduce_max_sync(m, v);
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(m, v, o, G));
+    return v;
+}
+template <int G>
+__device__ __forceinline__ int group_min(int v, unsigned m) {
+    if constexpr (G == 32) return __reduce_min_sync(m, v);
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(m, v, o, G));
+    return v;
+}
+
 }  // namespace
 
 template <int K, int G, int MODE>
@@ -122,8 +140,10 @@ __device__ __forceinline__ void w_windows(WState<K, G, MODE>& S, const uint32_t*
             S.HWb[r] = hw;
         }
     }
-    if (lane == 0) S.rv.init(pool, S.v_pos, S.vdir, a + 1, rv_r);
-    if (lane == G - 1) S.rh.init(pool, S.h_pos, S.hdir, b + K, rh_r);
+    // every lane of the group keeps both readers (same words, one transaction):
+    // refills and feeds are then straight-line selects, not lane-0 branches
+    S.rv.init(pool, S.v_pos, S.vdir, a + 1, rv_r);
+    S.rh.init(pool, S.h_pos, S.hdir, b + K, rh_r);
 }
 
 // Table modes: sentinel bytes over slots whose v or h symbol lies past the
@@ -175,20 +195,16 @@ __device__ __forceinline__ void wfeed(WState<K, G, MODE>& S, int lane, unsigned 
         if constexpr (ODD) {  // v: slot k <- k-1, new symbol at slot 0 (lane 0's reader)
             const uint32_t out = (S.VW[NW - 1] >> top) & 3u;
             uint32_t in = __shfl_up_sync(m, out, 1, G);
-            if (lane == 0) {
-                in = S.rv.cur >> 30;
-                S.rv.cur <<= 2;
-            }
+            in = lane == 0 ? S.rv.cur >> 30 : in;
+            S.rv.cur <<= 2;
 #pragma unroll
             for (int w = NW - 1; w > 0; --w) S.VW[w] = __funnelshift_l(S.VW[w - 1], S.VW[w], 2);
             S.VW[0] = (S.VW[0] << 2) | in;
         } else {  // h: slot k <- k+1, new symbol at slot K-1 (lane G-1's reader)
             const uint32_t out = S.HW[0] & 3u;
             uint32_t in = __shfl_down_sync(m, out, 1, G);
-            if (lane == G - 1) {
-                in = S.rh.cur & 3u;
-                S.rh.cur >>= 2;
-            }
+            in = lane == G - 1 ? S.rh.cur & 3u : in;
+            S.rh.cur >>= 2;
 #pragma unroll
             for (int w = 0; w < NW - 1; ++w) S.HW[w] = __funnelshift_r(S.HW[w], S.HW[w + 1], 2);
             const uint32_t keep = top == 30 ? 0xFFFFFFFFu : ((1u << (top + 2)) - 1u);
@@ -200,14 +216,16 @@ __device__ __forceinline__ void wfeed(WState<K, G, MODE>& S, int lane, unsigned 
         if constexpr (ODD) {
             const uint32_t out = (S.VWb[NB - 1] >> top) & 0xFFu;
             uint32_t in = __shfl_up_sync(m, out, 1, G);
-            if (lane == 0) in = S.rv.take();
+            const uint32_t own = S.rv.take();
+            in = lane == 0 ? own : in;
 #pragma unroll
             for (int r = NB - 1; r > 0; --r) S.VWb[r] = __funnelshift_l(S.VWb[r - 1], S.VWb[r], 8);
             S.VWb[0] = (S.VWb[0] << 8) | in;
         } else {
             const uint32_t out = S.HWb[0] & 0xFFu;
             uint32_t in = __shfl_down_sync(m, out, 1, G);
-            if (lane == G - 1) in = S.rh.take();
+            const uint32_t own = S.rh.take();
+            in = lane == G - 1 ? own : in;
 #pragma unroll
             for (int r = 0; r < NB - 1; ++r) S.HWb[r] = __funnelshift_r(S.HWb[r], S.HWb[r + 1], 8);
             const uint32_t keep = top == 24 ? 0xFFFFFFFFu : ((1u << (top + 8)) - 1u);
@@ -484,15 +502,19 @@ __device__ __forceinline__ void wstep(WState<K, G, MODE>& S, int32_t (&cur)[K / 
             : "r"(cand[s]), "r"(c), "r"(P.zero), "r"(P.one), "n"(kDeadS), "r"(1u << (s & 31)));
     }
     // running best (align.cpp:123-127): strict improvement, first cell wins:
-    // the highest lane holding the maximum, its highest slot holding it
-    // (group-uniform branch: both reductions on the group's mask)
-    if (gmax - X > S.Tv) {
-        const unsigned bal = __ballot_sync(gmask, mv == gmax);
-        const int bl = 31 - __clz(bal) - (threadIdx.x & 31 & ~(G - 1));
-        const int bs = __shfl_sync(gmask, mk & 63, bl, G);
-        S.Tv = gmax - X;
-        S.best_d = d;
-        S.best_u = S.ubase + bl * SS + bs;
+    // the highest lane holding the maximum, its highest slot holding it.
+    // Branch-free (a group-divergent branch here stalled the lockstep warp
+    // on branch resolution at most steps): the ballot and the shuffle run
+    // every step and the update is a select.
+    {
+        const bool improve = gmax - X > S.Tv;
+        const unsigned bal = __ballot_sync(fm, mv == gmax);
+        const unsigned gb = G == 32 ? bal : (bal >> (threadIdx.x & 31 & ~(G - 1))) & ((1u << (G & 31)) - 1u);
+        const int bl = 31 - __clz(gb);
+        const int bs = __shfl_sync(fm, mk & 63, bl, G);
+        S.best_u = improve ? S.ubase + bl * SS + bs : S.best_u;
+        S.best_d = improve ? d : S.best_d;
+        S.Tv = improve ? gmax - X : S.Tv;
     }
 #pragma unroll
     for (int s = 0; s < SS; ++s) cur[s] = kept[s];
@@ -503,8 +525,8 @@ __device__ __forceinline__ void wstep(WState<K, G, MODE>& S, int32_t (&cur)[K / 
         const uint32_t lv = ~dm & vml;
         const int hs_l = lv ? k0 + wbfind(lv) : -1;
         const int ls_l = lv ? k0 + __ffs(lv) - 1 : kBig;
-        const int hs = __reduce_max_sync(gmask, hs_l);
-        const int ls = __reduce_min_sync(gmask, ls_l);
+        const int hs = group_max<G>(hs_l, fm);
+        const int ls = group_min<G>(ls_l, fm);
         S.hs1 = hs;
         S.lr1 = hs < 0 ? -1 : KB - ls;
     }
@@ -721,8 +743,8 @@ __global__ void __launch_bounds__(32 * kWideWarps, wide_min_blocks<K, G, MODE>()
             continue;
         }
         if (active && (it & (PER - 1)) == 0) {  // the same iteration for every group
-            if (lane == 0) S.rv.refill(P.pool);
-            if (lane == G - 1) S.rh.refill(P.pool);
+            S.rv.refill(P.pool);
+            S.rh.refill(P.pool);
         }
         wstep<K, G, MODE, true, true>(S, O, E, P, tab, gap, X, it, lane, gmask, sk, srow);
         wstep<K, G, MODE, false, true>(S, E, O, P, tab, gap, X, it, lane, gmask, sk, srow);
