@@ -12,7 +12,7 @@ SRCS_CU := $(CSRC)/xb_kernels.cu $(CSRC)/xb_thread.cu $(CSRC)/xb_group.cu $(CSRC
 SRCS_CPP := $(CSRC)/xb_synth.cpp $(CSRC)/xb_ingest.cpp
 HDRS := $(CSRC)/xb_internal.h $(CSRC)/xb_kernels.cuh include/xdrop_b200.h
 
-all: lib oracle
+all: lib oracle checked
 
 # parallel object builds: make -j lib
 
@@ -63,7 +63,7 @@ $(CHK_LIB): $(CHKDIR)/xb_kernels.o $(CHKDIR)/xb_thread.o $(CHKDIR)/xb_group.o $(
 	@mkdir -p $(dir $(CHK_LIB))
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^ -lcudadevrt -lpthread
 
-oracle:
+oracle: lib
 	$(MAKE) -s -C oracle liboracle.so
 	@if [ -d /root/reference/proj/src ]; then $(MAKE) -s -C oracle ref; fi
 
