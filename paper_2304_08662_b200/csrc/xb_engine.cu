@@ -1239,7 +1239,9 @@ static int run_plan(xb_batch* B, DevBatch& D) {
     const int default_start = latency_mode ? 2 : 4;
     tp.pilot_n = pn;
     tp.pilot_stride = pn ? std::max<long long>(1, nu / pn) : 1;
-    tp.pilot_cap = 1024;
+    // 512 antidiagonals: config 5 and 4 keep their start tiers (K24, K64; 256 sent config 4
+    // to K48 at a third of the rate), the pilot on a config-5 shard of 8 takes 0.08 ms, not 0.29
+    tp.pilot_cap = std::getenv("XB_PILOT_CAP") ? std::atoi(std::getenv("XB_PILOT_CAP")) : 512;
     tp.pilot_w = D.d_pilot;
     tp.esc_to_warp = (B->flags & XB_FLAG_ESC_TO_WARP) ? 1 : 0;
     for (int t = 0; t < kWarpTier; ++t) {
