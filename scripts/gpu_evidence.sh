@@ -1,18 +1,16 @@
-# Round-2 evidence: tests, smoke, bench + reference arm, launch list (ncu), full ncu of the
-# K24 start tier, the wide tier at X = 100, the per-config report, shard balance.  Every ncu run
-# under its own timeout (ncu serialises kernels); .ncu-rep files are summarised to text and
-# removed (gpurun_out/ must stay under 64 MiB to come back).
+# Round-2 evidence: tests (product and bounds-checked builds), smoke, bench + reference arm,
+# launch list (ncu), full ncu of the K24 start tier and of the wide K128 tier, the per-config
+# report.  Every ncu run under its own timeout; .ncu-rep files are summarised and removed
+# (gpurun_out/ must stay under 64 MiB to come back).
 mkdir -p gpurun_out
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
 timeout 1500 python -m pytest tests -x -q -m gpu 2>&1 | tail -2
+XB_LIB_PATH=$PWD/paper_2304_08662_b200/_lib/libxdrop_b200_checked.so timeout 2400 python -m pytest tests -q -m gpu -k "not full_size_every_row" 2>&1 | tail -2
 timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.log; echo "bench rc=$?"
 timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.log; echo "ref rc=$?"
 timeout 900 python bench.py --config 4 --x 100 --steps 3 --warmup 3 --e2e-steps 2 --no-cpu-baseline > gpurun_out/bench_c4x100.json 2> gpurun_out/bench_c4x100.log; echo "bench c4x100 rc=$?"
 timeout 600 python bench.py --steps 2 --warmup 1 --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_plain.json 2>/dev/null && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --e2e-steps 1 > gpurun_out/ncu_launches.log 2>&1; echo "ncu-launches rc=$?"
-timeout 600 python scripts/prof_run.py --config 5 --scale 1.0 --runs 1 > gpurun_out/prof_full_plain.log 2>&1 && \
-timeout 1200 ncu --set full --clock-control none --kernel-name-base mangled -k regex:thread_tier_kernelILi24ELi0E -c 1 -o gpurun_out/prof_main python scripts/prof_run.py --config 5 --scale 1.0 --runs 1 > gpurun_out/ncu_main.log 2>&1; echo "ncu-main rc=$?"
-python scripts/ncu_summary.py report gpurun_out/prof_main.ncu-rep gpurun_out/r2_thread_k24_config5_full.txt; rm -f gpurun_out/prof_main.ncu-rep
 timeout 1200 ncu --set full --clock-control none --kernel-name-base mangled -k regex:wide_tier_kernelILi128ELi8ELi0E -c 1 -o gpurun_out/prof_wide python scripts/prof_run.py --config 4 --scale 1.0 --x 100 --runs 1 > gpurun_out/ncu_wide.log 2>&1; echo "ncu-wide rc=$?"
 python scripts/ncu_summary.py report gpurun_out/prof_wide.ncu-rep gpurun_out/r2_wide_k128_config4_x100.txt; rm -f gpurun_out/prof_wide.ncu-rep
 timeout 1500 python scripts/config_report.py --out gpurun_out/r2_configs > gpurun_out/configs.log 2>&1; echo "configs rc=$?"

@@ -1,5 +1,6 @@
 mkdir -p gpurun_out
-for cap in 1024 512 256; do
-echo "cap $cap"
-for a in "--config 5 --scale 1.0 --shard 0/8" "--config 5 --scale 1.0" "--config 4 --scale 1.0" "--config 4 --scale 1.0 --x 100" "--config 5 --scale 0.5 --x 40"; do XB_PILOT_CAP=$cap timeout 300 python scripts/prof_run.py --runs 2 $a | grep -o "start tier [0-9]*\|prep [0-9.]* ms, pilot [0-9.]* ms, GCUPS [0-9.]*" | tr '\n' ' '; echo; done
-done
+timeout 300 python scripts/lat_probe.py --configs 2 --alone-only --settings g2 > gpurun_out/lat.log 2>&1; cat gpurun_out/lat.log
+T=$(python -c "import json;print(json.loads(open('gpurun_out/lat.log').readline())['longest_task'])")
+timeout 900 ncu --set full --import-source on --clock-control none --kernel-name-base mangled -k regex:group_tier_kernelILi32ELi4ELi0E -c 1 -o gpurun_out/gsrc python scripts/lat_probe.py --configs 2 --alone-only --task $T --settings g2 > gpurun_out/ncu_gsrc.log 2>&1; echo "ncu rc=$?"
+ncu -i gpurun_out/gsrc.ncu-rep --page source --csv --print-source sass > gpurun_out/gsrc.csv 2>/dev/null
+python scripts/ncu_summary.py report gpurun_out/gsrc.ncu-rep gpurun_out/r2_group_k32_c2_alone.txt; rm -f gpurun_out/gsrc.ncu-rep
