@@ -911,14 +911,21 @@ static Workspace* acquire_workspace(int dev) {
 }
 
 // The sequences a device's batch references (tasks: this device's shard;
-// units mode: its units), or an empty vector when the batch is dense enough
-// in references (every sequence in several tasks) that the whole pool is
-// needed anyway -- then the scan is skipped and the image goes up whole.
+// units mode: its units), or an empty vector when the device already holds
+// the whole pool.  The scan is a relaxed byte store per reference on all
+// host threads (~0.5 ms for config 5's 4M references); a dense batch is no
+// sign of a full one (a rank's locality shard references every sequence of
+// its part of the pool many times, and only that part).
 static void referenced_sequences(const xb_batch* B, const DevBatch& D, const void* items,
                                  std::vector<uint8_t>& need) {
-    const int64_t ns = int64_t(B->pool->seq_pos.size());
     need.clear();
-    if (ns == 0 || 2 * D.n_items >= 8 * ns) return;
+    int64_t ns = 0;
+    {
+        std::lock_guard<std::mutex> g(B->pool->mu);
+        ns = int64_t(B->pool->seq_pos.size());
+        auto it = B->pool->dev.find(D.dev);
+        if (ns == 0 || (it != B->pool->dev.end() && it->second.ready)) return;
+    }
     need.assign(size_t(ns), 0);
     uint8_t* m = need.data();
     const bool sh = !D.tasks.empty();

@@ -1,6 +1,4 @@
 mkdir -p gpurun_out
-timeout 300 python scripts/lat_probe.py --configs 2 --alone-only --settings g2 > gpurun_out/lat.log 2>&1; cat gpurun_out/lat.log
-T=$(python -c "import json;print(json.loads(open('gpurun_out/lat.log').readline())['longest_task'])")
-timeout 900 ncu --set full --import-source on --clock-control none --kernel-name-base mangled -k regex:group_tier_kernelILi32ELi4ELi0E -c 1 -o gpurun_out/gsrc python scripts/lat_probe.py --configs 2 --alone-only --task $T --settings g2 > gpurun_out/ncu_gsrc.log 2>&1; echo "ncu rc=$?"
-ncu -i gpurun_out/gsrc.ncu-rep --page source --csv --print-source sass > gpurun_out/gsrc.csv 2>/dev/null
-python scripts/ncu_summary.py report gpurun_out/gsrc.ncu-rep gpurun_out/r2_group_k32_c2_alone.txt; rm -f gpurun_out/gsrc.ncu-rep
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -m gpu -x -k "locality or residency or pool_grows or multi_device or batch_stream or config5" 2>&1 | tail -2
+XB_BENCH_FUNCTIONAL=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 2 --warmup 1 --e2e-steps 2 --no-cpu-baseline > gpurun_out/bench_n2.json 2> gpurun_out/bench_n2.err; echo "n2 strong rc=$?"
+timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench1.json 2> gpurun_out/bench1.err; echo "n1 rc=$?"
