@@ -1243,7 +1243,16 @@ static int run_plan(xb_batch* B, DevBatch& D) {
     // than an escalation, which re-runs the unit after the whole start tier.
     const long long pn = (forced >= 0 || (B->flags & XB_FLAG_GENERIC_ONLY) || latency_mode)
                              ? 0 : std::min<long long>(nu, 64 + nu / 512);
-    const int default_start = latency_mode ? 2 : 4;
+    // Latency-planned batches have no pilot (it would cost as much as the
+    // batch) and start at K32 lane groups, or at K16 for DNA with X <= 10.
+    // Measured: config 1 (X = 10) K16 0.223 ms, K24 0.239, K32 0.263, no
+    // escalations; configs 2 and 3 (X = 15, 20) are fastest at K32: at K24
+    // their few escalating units (38, 209) finish in the tail, 7.4 ms / 3.6 ms
+    // even with a concurrent consumer (whose polling slowed the start tier),
+    // against 6.4 / 3.4 ms.
+    int latency_start = (p->scheme.kind == 0 && p->scheme.x <= 10) ? 0 : 2;
+    if (const char* e = std::getenv("XB_LATENCY_START")) latency_start = std::atoi(e);
+    const int default_start = latency_mode ? latency_start : 4;
     tp.pilot_n = pn;
     tp.pilot_stride = pn ? std::max<long long>(1, nu / pn) : 1;
     // 512 antidiagonals: config 5 and 4 keep their start tiers (K24, K64; 256 sent config 4
@@ -1414,7 +1423,7 @@ static int run_cascade(xb_batch* B, DevBatch& D) {
     if (t0 < kWarpTier) {
         // ---- the start tier ----
         tp.tier = t0;
-        if (D.all_group || D.no_group) {
+        if (D.no_group || D.all_group) {
             tp.role = kRoleAll;
             int per_sm = D.all_group ? D.gocc[t0] : D.occ[t0];
             if (D.all_group && t0 < kNarrowTiers) per_sm = std::min(per_sm, latency_blocks_per_sm(D));

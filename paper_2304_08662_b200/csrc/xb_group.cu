@@ -791,10 +791,19 @@ __global__ void __launch_bounds__(128) group_tier_kernel(TierParams P) {
         run(std::true_type{});
     else
         run(std::false_type{});
-    if (P.pilot || lane != 0) return;
-    if (sk.units) atomicAdd(&P.ctr->units[P.tier], sk.units);
-    if (sk.cells) atomicAdd(&P.ctr->cells[P.tier], sk.cells);
-    if (sk.esc) atomicAdd(&P.ctr->escalated[P.tier], sk.esc);
+    if (P.pilot) return;
+    if (lane == 0) {
+        if (sk.units) atomicAdd(&P.ctr->units[P.tier], sk.units);
+        if (sk.cells) atomicAdd(&P.ctr->cells[P.tier], sk.cells);
+        if (sk.esc) atomicAdd(&P.ctr->escalated[P.tier], sk.esc);
+    }
+    if (P.role == kRoleStart) {  // a latency-planned start tier with a concurrent consumer
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            if (atomicAdd(&P.ctr->prod_done, 1u) == gridDim.x - 1) atomicExch(&P.ctr->prod_finished, 1);
+        }
+    }
 }
 
 #define XB_GINST(K, G)                                                     \

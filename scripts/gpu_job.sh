@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_parity.py -q -m gpu -x -k "locality or residency or pool_grows or multi_device or batch_stream or config5" 2>&1 | tail -2
-XB_BENCH_FUNCTIONAL=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 2 --warmup 1 --e2e-steps 2 --no-cpu-baseline > gpurun_out/bench_n2.json 2> gpurun_out/bench_n2.err; echo "n2 strong rc=$?"
-timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench1.json 2> gpurun_out/bench1.err; echo "n1 rc=$?"
+for c in 1 2 3; do timeout 300 python scripts/prof_run.py --config $c --scale 1.0 --runs 3 | grep -o "start tier [0-9]*\|tiers ms \[[^]]*\]\|GCUPS [0-9.]*" | tr '\n' ' '; echo; done
+timeout 1500 python -m pytest tests -q -m gpu -x 2>&1 | tail -2
