@@ -174,3 +174,24 @@ def test_package_blosum62_matches_reference_fixture():
     assert B.ALPHABET == a and list(B.CELLS) == list(c)
     m = xb.parse_submatrix(B.text())
     assert m.alphabet == a and list(m.cells) == list(c)
+
+
+def test_shard_tasks_validation_and_modes():
+    """xb_shard_tasks (host-only): both modes cover every task once, the
+    assignment is deterministic, and task errors mirror xb_extend_batch."""
+    ds = synth.make(5, 0.002)
+    pool = xb.DevicePool(xb.ScoringScheme.match_mismatch(1, -1, -1, ds.x), ds.symbols, ds.offsets)
+    for loc in (False, True):
+        a = xb.xband.shard_tasks(pool, ds.tasks, ds.k, 3, locality=loc)
+        b = xb.xband.shard_tasks(pool, ds.tasks, ds.k, 3, locality=loc)
+        assert (a == b).all() and set(np.unique(a)) == {0, 1, 2}
+        one = xb.xband.shard_tasks(pool, ds.tasks, ds.k, 1, locality=loc)
+        assert (one == 0).all()
+    bad = ds.tasks.copy()
+    bad[5, 0] = len(ds.offsets) + 10  # an unknown sequence
+    with pytest.raises(xb.DanglingReference):
+        xb.xband.shard_tasks(pool, bad, ds.k, 2)
+    bad = ds.tasks.copy()
+    bad[7, 2] = 10 ** 9  # a seed past its sequence
+    with pytest.raises(xb.SeedOutOfBounds):
+        xb.xband.shard_tasks(pool, bad, ds.k, 2, locality=True)
