@@ -1,2 +1,1 @@
-mkdir -p gpurun_out
-timeout 1200 python -m pytest tests/test_gpu_random.py -q -m gpu 2>&1 | tail -15
+A_LIB=$PWD/paper_2304_08662_b200/_lib/libxdrop_b200_A.so bash scripts/ab_run.sh "--config 5 --scale 1.0" "--config 4 --scale 1.0" "--config 5 --scale 0.5 --x 40"
