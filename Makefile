@@ -8,7 +8,7 @@ CSRC := paper_2304_08662_b200/csrc
 LIB := paper_2304_08662_b200/_lib/libxdrop_b200.so
 OBJDIR := build
 
-SRCS_CU := $(CSRC)/xb_kernels.cu $(CSRC)/xb_thread.cu $(CSRC)/xb_group.cu $(CSRC)/xb_wide.cu $(CSRC)/xb_engine.cu
+SRCS_CU := $(CSRC)/xb_kernels.cu $(CSRC)/xb_thread.cu $(CSRC)/xb_group.cu $(CSRC)/xb_lane.cu $(CSRC)/xb_wide.cu $(CSRC)/xb_engine.cu
 SRCS_CPP := $(CSRC)/xb_synth.cpp $(CSRC)/xb_ingest.cpp
 HDRS := $(CSRC)/xb_internal.h $(CSRC)/xb_kernels.cuh include/xdrop_b200.h
 
@@ -30,6 +30,10 @@ $(OBJDIR)/xb_group.o: $(CSRC)/xb_group.cu $(HDRS)
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(NVFLAGS) -dc -o $@ $< 2> $(OBJDIR)/xb_group.ptxas.txt || (cat $(OBJDIR)/xb_group.ptxas.txt; exit 1)
 
+$(OBJDIR)/xb_lane.o: $(CSRC)/xb_lane.cu $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -dc -o $@ $< 2> $(OBJDIR)/xb_lane.ptxas.txt || (cat $(OBJDIR)/xb_lane.ptxas.txt; exit 1)
+
 $(OBJDIR)/xb_wide.o: $(CSRC)/xb_wide.cu $(HDRS)
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(NVFLAGS) -dc -o $@ $< 2> $(OBJDIR)/xb_wide.ptxas.txt || (cat $(OBJDIR)/xb_wide.ptxas.txt; exit 1)
@@ -46,7 +50,7 @@ $(OBJDIR)/xb_ingest.o: $(CSRC)/xb_ingest.cpp include/xdrop_b200.h
 	@mkdir -p $(OBJDIR)
 	/usr/bin/g++ -O3 -std=c++17 -fPIC -Wall -c -o $@ $<
 
-$(LIB): $(OBJDIR)/xb_kernels.o $(OBJDIR)/xb_thread.o $(OBJDIR)/xb_group.o $(OBJDIR)/xb_wide.o $(OBJDIR)/xb_engine.o $(OBJDIR)/xb_synth.o $(OBJDIR)/xb_ingest.o
+$(LIB): $(OBJDIR)/xb_kernels.o $(OBJDIR)/xb_thread.o $(OBJDIR)/xb_group.o $(OBJDIR)/xb_lane.o $(OBJDIR)/xb_wide.o $(OBJDIR)/xb_engine.o $(OBJDIR)/xb_synth.o $(OBJDIR)/xb_ingest.o
 	@mkdir -p $(dir $(LIB))
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^ -lcudadevrt -lpthread
 
@@ -59,7 +63,7 @@ checked: $(CHK_LIB)
 $(CHKDIR)/%.o: $(CSRC)/%.cu $(HDRS)
 	@mkdir -p $(CHKDIR)
 	$(NVCC) $(NVFLAGS) -DXB_CHECKS=1 -dc -o $@ $< > /dev/null 2>&1 || $(NVCC) $(NVFLAGS) -DXB_CHECKS=1 -dc -o $@ $<
-$(CHK_LIB): $(CHKDIR)/xb_kernels.o $(CHKDIR)/xb_thread.o $(CHKDIR)/xb_group.o $(CHKDIR)/xb_wide.o $(CHKDIR)/xb_engine.o $(OBJDIR)/xb_synth.o $(OBJDIR)/xb_ingest.o
+$(CHK_LIB): $(CHKDIR)/xb_kernels.o $(CHKDIR)/xb_thread.o $(CHKDIR)/xb_group.o $(CHKDIR)/xb_lane.o $(CHKDIR)/xb_wide.o $(CHKDIR)/xb_engine.o $(OBJDIR)/xb_synth.o $(OBJDIR)/xb_ingest.o
 	@mkdir -p $(dir $(CHK_LIB))
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^ -lcudadevrt -lpthread
 

@@ -32,6 +32,8 @@ template <int K, int G, int MODE>
 __global__ void group_tier_kernel(TierParams P);
 template <int K, int G, int MODE>
 __global__ void wide_tier_kernel(TierParams P);
+template <int K, int G, int MODE>
+__global__ void lane_tier_kernel(TierParams P);
 template <int ENC>
 __global__ void warp_tier_kernel(TierParams P);
 __global__ void select_tier_kernel(TierParams P, int forced, int32_t* host_out);
@@ -1072,12 +1074,26 @@ static int upload_inputs(xb_batch* B, DevBatch& D, const void* items) {
     return XB_OK;
 }
 
-constexpr int kGroupLanes = 4;  // lanes per unit in the lane-group tiers
+constexpr int kGroupLanes = 4;  // lanes per unit in the lane-group tiers (xb_group.cu)
+constexpr int kLaneLanes = 8;   // lanes per unit in the lane tiers (xb_lane.cu)
+
+// Which kernels serve the several-lanes-per-unit launches of the narrow
+// tiers: the lane tiers (8 lanes per unit, short step) or the 4-lane groups.
+// XB_GROUP_FAMILY=4|8 overrides the choice (A/B runs).
+static bool use_lane_family() {
+    static const bool v = [] {
+        const char* e = std::getenv("XB_GROUP_FAMILY");
+        return e ? std::atoi(e) == 8 : false;
+    }();
+    return v;
+}
+static int group_lanes() { return use_lane_family() ? kLaneLanes : kGroupLanes; }
 
 template <bool GROUP, int K, int MODE>
 static void* tier_fn() {
     if constexpr (GROUP)
-        return reinterpret_cast<void*>(group_tier_kernel<K, kGroupLanes, MODE>);
+        return use_lane_family() ? reinterpret_cast<void*>(lane_tier_kernel<K, kLaneLanes, MODE>)
+                                 : reinterpret_cast<void*>(group_tier_kernel<K, kGroupLanes, MODE>);
     else
         return reinterpret_cast<void*>(thread_tier_kernel<K, MODE>);
 }
@@ -1274,7 +1290,7 @@ static int run_plan(xb_batch* B, DevBatch& D) {
         pp.pilot = 1;
         pp.role = kRoleAll;
         const bool g = !no_group;
-        const long long lanes = pn * (g ? kGroupLanes : 1);
+        const long long lanes = pn * (g ? group_lanes() : 1);
         const int blocks = int(std::min<long long>(D.sm_count * (g ? D.gocc[4] : D.occ[4]), (lanes + kTB - 1) / kTB));
         CK(cudaStreamWaitEvent(D.aux_stream, D.aux_ev[0], 0));
         CK(launch_tier(g, mode, 4, pp, blocks, D.aux_stream));
@@ -1307,19 +1323,21 @@ static int run_plan(xb_batch* B, DevBatch& D) {
 struct TailPlan {
     TierParams tp;                 // tier / role set per launch
     int32_t grid[kNumTiers];       // blocks for each tier's launch
-    int32_t group[kNumTiers];      // narrow tiers: 1 lane groups, 0 one thread per unit
+    int32_t group[kNumTiers];      // narrow tiers: 0 one thread per unit, 1 4-lane groups, 2 lane tiers
     int32_t mode;
     int32_t t0;
     int32_t warp_blocks, warp_threads, warp_enc;
 };
 
 template <int MODE>
-__device__ void tail_launch_tier(int t, bool group, const TierParams& P, int grid) {
+__device__ void tail_launch_tier(int t, int group, const TierParams& P, int grid) {
     const dim3 g = dim3(unsigned(grid)), b = dim3(kTB);
     switch (t) {
 #define XB_TAIL_NARROW(T, K)                                                                        \
     case T:                                                                                         \
-        if (group)                                                                                  \
+        if (group == 2)                                                                             \
+            lane_tier_kernel<K, kLaneLanes, MODE><<<g, b, 0, cudaStreamTailLaunch>>>(P);            \
+        else if (group)                                                                             \
             group_tier_kernel<K, kGroupLanes, MODE><<<g, b, 0, cudaStreamTailLaunch>>>(P);          \
         else                                                                                        \
             thread_tier_kernel<K, MODE><<<g, b, 0, cudaStreamTailLaunch>>>(P);                      \
@@ -1391,7 +1409,7 @@ constexpr int kConsumerBlocks = 4;
 // XB_LATENCY_BLOCKS overrides the choice (the sweep).
 static int latency_blocks_per_sm(const DevBatch& D) {
     if (const char* e = std::getenv("XB_LATENCY_BLOCKS")) return std::max(1, std::atoi(e));
-    const int64_t groups_per_block = kTB / kGroupLanes;
+    const int64_t groups_per_block = kTB / group_lanes();
     return D.n_units <= int64_t(D.sm_count) * groups_per_block ? 1 : 2;
 }
 
@@ -1427,7 +1445,15 @@ static int run_cascade(xb_batch* B, DevBatch& D) {
             tp.role = kRoleAll;
             int per_sm = D.all_group ? D.gocc[t0] : D.occ[t0];
             if (D.all_group && t0 < kNarrowTiers) per_sm = std::min(per_sm, latency_blocks_per_sm(D));
-            CK(launch_tier(D.all_group, mode, t0, tp, D.sm_count * per_sm, D.stream));
+            int blocks = D.sm_count * per_sm;
+            // one thread per unit: no more threads than units, so that a small
+            // batch fills whole warps on few SMSPs instead of a quarter of the
+            // lanes of every resident warp
+            if (const char* e = std::getenv("XB_THREAD_GRID_CAP"); e && !D.all_group && t0 < kNarrowTiers) {
+                const int cap = std::atoi(e);
+                blocks = int(std::min<int64_t>(blocks, cap > 1 ? cap : std::max<int64_t>(1, D.n_units / kTB)));
+            }
+            CK(launch_tier(D.all_group, mode, t0, tp, blocks, D.stream));
         } else {  // throughput: one thread per unit (or 8 lanes, wide), the concurrent consumer beside it
             if (concurrent) {
                 // the next tier's list starts empty-marked
@@ -1476,7 +1502,7 @@ static int run_cascade(xb_batch* B, DevBatch& D) {
                 // lane groups; in latency mode no more resident blocks than the start
                 // tier (their work is its long units)
                 plan.grid[t] = D.sm_count * (D.all_group ? std::min(D.gocc[t], latency_blocks_per_sm(D)) : D.gocc[t]);
-                plan.group[t] = 1;
+                plan.group[t] = use_lane_family() ? 2 : 1;
             }
         }
         // one warp per scratch slot: blocks of 4 warps, or one smaller block
