@@ -86,6 +86,8 @@ typedef struct {
 #define XB_FLAG_THROUGHPUT 128  /* plan a small batch like a large one: pilot + cost model (testing) */
 #define XB_FLAG_SERIAL_TAIL 4096 /* wider tiers only after the start tier (no concurrent escalation consumer; ablation) */
 #define XB_FLAG_LOCALITY 8192   /* multi-device batches: locality-aware shards (xb_shard_tasks XB_SHARD_LOCALITY) */
+#define XB_FLAG_LANES 16384     /* several-lanes-per-unit launches of the narrow tiers use the lane tiers (8 lanes per unit; testing) */
+#define XB_FLAG_NO_LANES 32768  /* ... never the lane tiers: the 4-lane groups (testing) */
 
 /* Per-call device statistics (summed over devices; times are the max).
  * Tiers: 0..4 = one unit per thread (or per 4-lane group) with a
@@ -109,7 +111,7 @@ typedef struct {
     int32_t start_tier;          /* tier the pilot chose */
     int64_t dbg[6];              /* [0..4] instrumented builds only (-DXB_COUNTERS=1), else 0;
                                     [5] units a lane-group tier resumed at an even antidiagonal */
-    int32_t start_lane_groups;   /* 1: the start tier ran as lane groups (latency-bound batch) */
+    int32_t start_lane_groups;   /* latency-bound batch: the start tier ran as 4-lane groups (1) or on the lane tiers (2) */
     int32_t reserved;
 } xb_stats;
 

@@ -37,6 +37,8 @@ XB_FLAG_NO_GROUP = 64
 XB_FLAG_THROUGHPUT = 128
 XB_FLAG_SERIAL_TAIL = 4096
 XB_FLAG_LOCALITY = 8192
+XB_FLAG_LANES = 16384
+XB_FLAG_NO_LANES = 32768
 
 XB_SHARD_LPT = 0
 XB_SHARD_LOCALITY = 1
@@ -80,7 +82,8 @@ def tier_kernel_name(t: int, stats: dict, flags: int = 0) -> str:
         return f"wide_k{TIER_WIDTHS[t]}"
     s = stats.get("start_tier", -1)
     group = bool(flags & 32) or (t == s and stats.get("start_lane_groups")) or (t > s >= 0 and not flags & 64)
-    return f"{'group' if group else 'thread'}_k{TIER_WIDTHS[t]}"
+    lanes = group and (stats.get("start_lane_groups") == 2 or flags & XB_FLAG_LANES)
+    return f"{'lane' if lanes else 'group' if group else 'thread'}_k{TIER_WIDTHS[t]}"
 
 
 class XbStats(C.Structure):
@@ -98,7 +101,7 @@ class XbStats(C.Structure):
                 "cells_tier": list(self.cells_tier), "escalated": list(self.escalated),
                 "h2d_bytes": self.h2d_bytes, "d2h_bytes": self.d2h_bytes,
                 "sm_count": self.sm_count, "start_tier": self.start_tier,
-                "dbg": list(self.dbg), "start_lane_groups": bool(self.start_lane_groups)}
+                "dbg": list(self.dbg), "start_lane_groups": int(self.start_lane_groups)}
 
 
 _lib = None

@@ -809,6 +809,7 @@ struct DevBatch {
     int32_t* h_misc = nullptr;
     TierParams tp{};           // planned launch parameters (run_plan -> run_cascade)
     bool all_group = false, no_group = false;
+    int group_fam = 1;  // several-lanes-per-unit launches of the narrow tiers: 1 = 4-lane groups, 2 = lane tiers
     Workspace* ws = nullptr;
     DevPool* pool = nullptr;
     std::vector<int64_t> tasks;  // global task (or unit) indices of this shard
@@ -831,6 +832,7 @@ struct DevBatch {
     int sm_count = 0;
     int occ[kWarpTier] = {};   // resident blocks per SM: thread kernels (0-4), wide kernels (5-8)
     int gocc[kWarpTier] = {};  // lane-group kernels (0-4), one-warp-per-unit wide kernels (5-9)
+    int locc[kWarpTier] = {};  // lane-tier kernels (0-4)
     int mode = 0;
     int launches = 0;
     // host staging (pinned)
@@ -1076,36 +1078,40 @@ static int upload_inputs(xb_batch* B, DevBatch& D, const void* items) {
 
 constexpr int kGroupLanes = 4;  // lanes per unit in the lane-group tiers (xb_group.cu)
 constexpr int kLaneLanes = 8;   // lanes per unit in the lane tiers (xb_lane.cu)
+static int family_lanes(int fam) { return fam == 2 ? kLaneLanes : fam == 1 ? kGroupLanes : 1; }
 
-// Which kernels serve the several-lanes-per-unit launches of the narrow
-// tiers: the lane tiers (8 lanes per unit, short step) or the 4-lane groups.
+// Kernel families of the narrow tiers (K16..K64): 0 = one thread per unit,
+// 1 = 4-lane groups (xb_group.cu), 2 = lane tiers (8 lanes per unit,
+// xb_lane.cu).  The lane tiers step a lone unit ~1.6x sooner at ~2.5x the
+// instructions per unit and antidiagonal, so they take the batches that are
+// pure latency: few enough units that every SMSP holds at most one warp.
 // XB_GROUP_FAMILY=4|8 overrides the choice (A/B runs).
-static bool use_lane_family() {
-    static const bool v = [] {
+static int forced_group_family() {
+    static const int v = [] {
         const char* e = std::getenv("XB_GROUP_FAMILY");
-        return e ? std::atoi(e) == 8 : false;
+        return e ? (std::atoi(e) == 8 ? 2 : 1) : 0;
     }();
     return v;
 }
-static int group_lanes() { return use_lane_family() ? kLaneLanes : kGroupLanes; }
 
-template <bool GROUP, int K, int MODE>
+template <int FAM, int K, int MODE>
 static void* tier_fn() {
-    if constexpr (GROUP)
-        return use_lane_family() ? reinterpret_cast<void*>(lane_tier_kernel<K, kLaneLanes, MODE>)
-                                 : reinterpret_cast<void*>(group_tier_kernel<K, kGroupLanes, MODE>);
+    if constexpr (FAM == 2)
+        return reinterpret_cast<void*>(lane_tier_kernel<K, kLaneLanes, MODE>);
+    else if constexpr (FAM == 1)
+        return reinterpret_cast<void*>(group_tier_kernel<K, kGroupLanes, MODE>);
     else
         return reinterpret_cast<void*>(thread_tier_kernel<K, MODE>);
 }
 
-template <bool GROUP, int MODE>
+template <int FAM, int MODE>
 static void* tier_fn_t(int t) {
     switch (t) {
-        case 0: return tier_fn<GROUP, 16, MODE>();
-        case 1: return tier_fn<GROUP, 24, MODE>();
-        case 2: return tier_fn<GROUP, 32, MODE>();
-        case 3: return tier_fn<GROUP, 48, MODE>();
-        default: return tier_fn<GROUP, 64, MODE>();
+        case 0: return tier_fn<FAM, 16, MODE>();
+        case 1: return tier_fn<FAM, 24, MODE>();
+        case 2: return tier_fn<FAM, 32, MODE>();
+        case 3: return tier_fn<FAM, 48, MODE>();
+        default: return tier_fn<FAM, 64, MODE>();
     }
 }
 
@@ -1124,24 +1130,26 @@ static void* wide_fn_t(int t, bool latency) {
     }
 }
 
-// tiers 0-4: thread (or lane-group) kernels; 5-8: the wide one-warp-per-unit kernels
-static void* tier_kernel(bool group, int mode, int t) {
-    if (t >= kWideFirst)  // `group` selects the latency form (one warp per unit)
-        return mode == 0 ? wide_fn_t<0>(t, group) : mode == 1 ? wide_fn_t<1>(t, group) : wide_fn_t<2>(t, group);
-    if (group) return mode == 0 ? tier_fn_t<true, 0>(t) : mode == 1 ? tier_fn_t<true, 1>(t) : tier_fn_t<true, 2>(t);
-    return mode == 0 ? tier_fn_t<false, 0>(t) : mode == 1 ? tier_fn_t<false, 1>(t) : tier_fn_t<false, 2>(t);
+// tiers 0-4: the kernel of family `fam`; 5-9: the wide kernels, where any
+// fam != 0 selects the latency form (one warp per unit)
+static void* tier_kernel(int fam, int mode, int t) {
+    if (t >= kWideFirst)
+        return mode == 0 ? wide_fn_t<0>(t, fam != 0) : mode == 1 ? wide_fn_t<1>(t, fam != 0) : wide_fn_t<2>(t, fam != 0);
+    if (fam == 2) return mode == 0 ? tier_fn_t<2, 0>(t) : mode == 1 ? tier_fn_t<2, 1>(t) : tier_fn_t<2, 2>(t);
+    if (fam == 1) return mode == 0 ? tier_fn_t<1, 0>(t) : mode == 1 ? tier_fn_t<1, 1>(t) : tier_fn_t<1, 2>(t);
+    return mode == 0 ? tier_fn_t<0, 0>(t) : mode == 1 ? tier_fn_t<0, 1>(t) : tier_fn_t<0, 2>(t);
 }
 
-static cudaError_t launch_tier(bool group, int mode, int t, const TierParams& P, int blocks,
+static cudaError_t launch_tier(int fam, int mode, int t, const TierParams& P, int blocks,
                                cudaStream_t st) {
     TierParams q = P;
     void* args[] = {&q};
-    return cudaLaunchKernel(tier_kernel(group, mode, t), dim3(unsigned(blocks)), dim3(kTB), args, 0, st);
+    return cudaLaunchKernel(tier_kernel(fam, mode, t), dim3(unsigned(blocks)), dim3(kTB), args, 0, st);
 }
 
-static int occupancy_blocks(bool group, int t, int mode, int* out) {
+static int occupancy_blocks(int fam, int t, int mode, int* out) {
     int b = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, tier_kernel(group, mode, t), kTB, 0) != cudaSuccess)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, tier_kernel(fam, mode, t), kTB, 0) != cudaSuccess)
         return XB_E_CUDA;
     *out = std::max(1, b);
     return XB_OK;
@@ -1277,8 +1285,9 @@ static int run_plan(xb_batch* B, DevBatch& D) {
     tp.pilot_w = D.d_pilot;
     tp.esc_to_warp = (B->flags & XB_FLAG_ESC_TO_WARP) ? 1 : 0;
     for (int t = 0; t < kWarpTier; ++t) {
-        if (!D.occ[t]) CK(occupancy_blocks(false, t, mode, &D.occ[t]) ? cudaErrorUnknown : cudaSuccess);
-        if (!D.gocc[t]) CK(occupancy_blocks(true, t, mode, &D.gocc[t]) ? cudaErrorUnknown : cudaSuccess);
+        if (!D.occ[t]) CK(occupancy_blocks(0, t, mode, &D.occ[t]) ? cudaErrorUnknown : cudaSuccess);
+        if (!D.gocc[t]) CK(occupancy_blocks(1, t, mode, &D.gocc[t]) ? cudaErrorUnknown : cudaSuccess);
+        if (!D.locc[t]) CK(occupancy_blocks(2, t, mode, &D.locc[t]) ? cudaErrorUnknown : cudaSuccess);
     }
     if (pn > 0) {
         // The pilot samples a stride of the units in input order (d_vals is
@@ -1290,10 +1299,10 @@ static int run_plan(xb_batch* B, DevBatch& D) {
         pp.pilot = 1;
         pp.role = kRoleAll;
         const bool g = !no_group;
-        const long long lanes = pn * (g ? group_lanes() : 1);
+        const long long lanes = pn * (g ? kGroupLanes : 1);
         const int blocks = int(std::min<long long>(D.sm_count * (g ? D.gocc[4] : D.occ[4]), (lanes + kTB - 1) / kTB));
         CK(cudaStreamWaitEvent(D.aux_stream, D.aux_ev[0], 0));
-        CK(launch_tier(g, mode, 4, pp, blocks, D.aux_stream));
+        CK(launch_tier(g ? 1 : 0, mode, 4, pp, blocks, D.aux_stream));
         CK(cudaEventRecord(D.aux_ev[1], D.aux_stream));
         CK(cudaStreamWaitEvent(D.stream, D.aux_ev[1], 0));
         ++D.launches;
@@ -1307,6 +1316,13 @@ static int run_plan(xb_batch* B, DevBatch& D) {
     D.tp = tp;
     D.all_group = all_group;
     D.no_group = no_group;
+    // a latency-planned batch that puts at most one lane-tier warp on every
+    // SMSP runs on the lane tiers (config 1: 0.217 -> 0.139 ms); larger ones
+    // are bound by instruction issue, where the 4-lane groups cost less
+    // (config 3: 3.4 ms against 3.8 ms, config 2: 6.4 against 11 ms)
+    D.group_fam = (B->flags & XB_FLAG_LANES) ? 2 : (B->flags & XB_FLAG_NO_LANES) ? 1
+                  : forced_group_family() ? forced_group_family()
+                  : (latency_mode && nu <= int64_t(D.sm_count) * (kTB / kLaneLanes)) ? 2 : 1;
     D.t0 = forced >= 0 ? forced : (pn > 0 ? -1 : default_start);  // -1: read back after the pilot
     return XB_OK;  // a pilot-chosen start tier arrives in h_misc[kMiscStartTier] (written by the kernel)
 }
@@ -1409,7 +1425,7 @@ constexpr int kConsumerBlocks = 4;
 // XB_LATENCY_BLOCKS overrides the choice (the sweep).
 static int latency_blocks_per_sm(const DevBatch& D) {
     if (const char* e = std::getenv("XB_LATENCY_BLOCKS")) return std::max(1, std::atoi(e));
-    const int64_t groups_per_block = kTB / group_lanes();
+    const int64_t groups_per_block = kTB / family_lanes(D.group_fam);
     return D.n_units <= int64_t(D.sm_count) * groups_per_block ? 1 : 2;
 }
 
@@ -1443,7 +1459,8 @@ static int run_cascade(xb_batch* B, DevBatch& D) {
         tp.tier = t0;
         if (D.no_group || D.all_group) {
             tp.role = kRoleAll;
-            int per_sm = D.all_group ? D.gocc[t0] : D.occ[t0];
+            const int* gocc = D.group_fam == 2 && t0 < kNarrowTiers ? D.locc : D.gocc;
+            int per_sm = D.all_group ? gocc[t0] : D.occ[t0];
             if (D.all_group && t0 < kNarrowTiers) per_sm = std::min(per_sm, latency_blocks_per_sm(D));
             int blocks = D.sm_count * per_sm;
             // one thread per unit: no more threads than units, so that a small
@@ -1453,7 +1470,7 @@ static int run_cascade(xb_batch* B, DevBatch& D) {
                 const int cap = std::atoi(e);
                 blocks = int(std::min<int64_t>(blocks, cap > 1 ? cap : std::max<int64_t>(1, D.n_units / kTB)));
             }
-            CK(launch_tier(D.all_group, mode, t0, tp, blocks, D.stream));
+            CK(launch_tier(D.all_group ? D.group_fam : 0, mode, t0, tp, blocks, D.stream));
         } else {  // throughput: one thread per unit (or 8 lanes, wide), the concurrent consumer beside it
             if (concurrent) {
                 // the next tier's list starts empty-marked
@@ -1464,7 +1481,7 @@ static int run_cascade(xb_batch* B, DevBatch& D) {
             tp.role = kRoleStart;
             // leave the consumer's blocks room to be resident whichever kernel
             // the hardware dispatches first (start-tier blocks are persistent)
-            CK(launch_tier(false, mode, t0, tp,
+            CK(launch_tier(0, mode, t0, tp,
                            std::max(1, D.sm_count * D.occ[t0] - (concurrent ? kConsumerBlocks : 0)), D.stream));
             if (concurrent) {
                 // a few high-priority blocks take the start tier's escalations while
@@ -1476,7 +1493,7 @@ static int run_cascade(xb_batch* B, DevBatch& D) {
                 TierParams cp = tp;
                 cp.tier = t0 + 1;
                 cp.role = kRoleConsumer;
-                CK(launch_tier(true, mode, t0 + 1, cp, kConsumerBlocks, D.aux_stream));
+                CK(launch_tier(1, mode, t0 + 1, cp, kConsumerBlocks, D.aux_stream));
                 CK(cudaEventRecord(D.aux_ev[1], D.aux_stream));
                 ++D.launches;
             }
@@ -1501,8 +1518,10 @@ static int run_cascade(xb_batch* B, DevBatch& D) {
             } else {
                 // lane groups; in latency mode no more resident blocks than the start
                 // tier (their work is its long units)
-                plan.grid[t] = D.sm_count * (D.all_group ? std::min(D.gocc[t], latency_blocks_per_sm(D)) : D.gocc[t]);
-                plan.group[t] = use_lane_family() ? 2 : 1;
+                const int fam = D.all_group ? D.group_fam : 1;
+                const int occ = fam == 2 ? D.locc[t] : D.gocc[t];
+                plan.grid[t] = D.sm_count * (D.all_group ? std::min(occ, latency_blocks_per_sm(D)) : occ);
+                plan.group[t] = fam;
             }
         }
         // one warp per scratch slot: blocks of 4 warps, or one smaller block
@@ -1880,7 +1899,7 @@ int xb_batch_stats(xb_batch* B, xb_stats* st) {
             st->escalated[t] += int64_t(c.escalated[t]);
         }
         st->start_tier = c.start_tier;
-        st->start_lane_groups = (D.n_units && D.all_group) ? 1 : 0;
+        st->start_lane_groups = (D.n_units && D.all_group) ? D.group_fam : 0;
         for (int q = 0; q < 6; ++q) st->dbg[q] += int64_t(c.dbg[q]);
         st->launches += D.launches + int(c.dbg[6]);  // host launches + the tail's device launches
         st->sm_count = D.sm_count;

@@ -158,7 +158,7 @@ def main():
             "gcups_paper": paper_products / (best / 1e3) / 1e9,
             "e2e_ms": 1e3 * min(e2e), "e2e_gcups": cells / min(e2e) / 1e9,
             "start_tier": (f"k{[16, 24, 32, 48, 64][st['start_tier']]} "
-                           + ("lane groups" if st["start_lane_groups"] else "thread/unit"))
+                           + ("lane tiers (8 lanes)" if st["start_lane_groups"] == 2 else "lane groups" if st["start_lane_groups"] else "thread/unit"))
             if 0 <= st["start_tier"] < 5 else None,
             "tier_ms": [round(v, 3) for v in st["ms_tier"]], "escalated": st["escalated"],
             "ref_tasks_compared": int(len(sel)), "ref_rows_equal": int(eq.sum()),

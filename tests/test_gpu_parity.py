@@ -59,11 +59,16 @@ def _by_scheme(entries):
 # 128 = THROUGHPUT (pilot + cost model even for a small batch)
 # 8 | t << 8 with t = WIDE_FIRST..: start on the wide tiers (8-32 lanes per unit, K96..K1024)
 from paper_2304_08662_b200.capi import NUM_TIERS, TIER_WIDTHS, WARP_TIER, WIDE_FIRST  # noqa: E402
+# 16384 = LANES (lane tiers, 8 lanes per unit), 32768 = NO_LANES (4-lane groups): small
+# batches pick the lane tiers by themselves, so both families are forced here
+LANES, NO_LANES = 16384, 32768
 TIER_FLAGS = ([0, 2, 128, 128 | 64] + [64 | 8 | (t << 8) for t in range(5)]
-              + [32 | 8 | (t << 8) for t in range(5)] + [8 | (t << 8) for t in range(WIDE_FIRST, WARP_TIER)])
+              + [32 | 8 | (t << 8) | NO_LANES for t in range(5)] + [32 | 8 | (t << 8) | LANES for t in range(5)]
+              + [8 | (t << 8) for t in range(WIDE_FIRST, WARP_TIER)])
 TIER_IDS = (["auto", "warp_tier_only", "pilot_cascade", "thread_pilot_cascade"]
             + [f"thread_k{w}" for w in (16, 24, 32, 48, 64)]
             + [f"group_k{w}" for w in (16, 24, 32, 48, 64)]
+            + [f"lane_k{w}" for w in (16, 24, 32, 48, 64)]
             + [f"wide_k{w}" for w in TIER_WIDTHS[WIDE_FIRST:]])
 
 
@@ -143,10 +148,11 @@ def _config_pool(xb, ds):
 
 
 @pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
-@pytest.mark.parametrize("flags", [0, 1, 2, 128, 128 | 64, 32, 64 | 8, 64 | 8 | (2 << 8), 32 | 8,
-                                   32 | 8 | (2 << 8)],
+@pytest.mark.parametrize("flags", [0, 1, 2, 128, 128 | 64, 32 | NO_LANES, 64 | 8, 64 | 8 | (2 << 8), 32 | 8 | NO_LANES,
+                                   32 | 8 | (2 << 8) | NO_LANES, 32 | LANES, 32 | 8 | LANES, 32 | 8 | (2 << 8) | LANES],
                          ids=["auto", "unsorted", "warp_tier_only", "pilot_cascade", "thread_cascade", "group_cascade",
-                              "thread_from_k16", "thread_from_k32", "group_from_k16", "group_from_k32"])
+                              "thread_from_k16", "thread_from_k32", "group_from_k16", "group_from_k32",
+                              "lane_cascade", "lane_from_k16", "lane_from_k32"])
 def test_configs_vs_reference_golden(xb, cfg, flags):
     from paper_2304_08662_b200 import synth
     meta = load_json("configs_meta.json")[str(cfg)]
@@ -182,7 +188,7 @@ def test_configs_sample_vs_oracle_full_size(xb, oracle, cfg):
     # escalations resume from saved records (past the record capacity on config 5);
     # K16 starts whose escalations a concurrent consumer takes while the start
     # tier runs (8: most units escalate) and the serial tail (4096)
-    for flags in (1, 32, 64, 64 | 8, 32 | 8, 8, 4096, 8 | 4096):
+    for flags in (1, 32 | NO_LANES, 32 | LANES, 64, 64 | 8, 32 | 8 | NO_LANES, 32 | 8 | LANES, 8, 4096, 8 | 4096):
         b, _ = xb.extend_tasks(pool, ds.tasks, ds.k, ds.band, exec_flags=flags)
         assert result_rows_equal(a, b).all(), flags
     # every sampled row inside the full run equals the sampled run
@@ -224,8 +230,9 @@ def test_self_extension_full_length(xb):
     assert len(set(right["delta_w"].tolist())) == 1
 
 
-@pytest.mark.parametrize("flags", [0, 32, 128 | 64, 64 | 8, 32 | 8],
-                         ids=["auto", "group", "thread_pilot", "thread_from_k16", "group_from_k16"])
+@pytest.mark.parametrize("flags", [0, 32 | NO_LANES, 128 | 64, 64 | 8, 32 | 8 | NO_LANES, 32 | LANES, 32 | 8 | LANES],
+                         ids=["auto", "group", "thread_pilot", "thread_from_k16", "group_from_k16", "lane",
+                              "lane_from_k16"])
 def test_band_failures_and_escalation(xb, oracle, flags):
     """Wide windows: X large so spreads exceed 32 and 64 slots (tier escalation)
     and a band small enough that some sides fail with exact spread/cells."""
@@ -255,8 +262,8 @@ def test_band_failures_and_escalation(xb, oracle, flags):
         even_resumes += xb.xband.last_stats()["dbg"][5]
         for q, (h, v) in enumerate(entries):
             assert rec_tuple(out[q]) == rec_tuple(oracle.extend(h, v, so, band)), (x, band, q)
-    if flags == 32 | 8:
-        # lane-group tiers from K16 up: records written at even antidiagonals
+    if flags & ~(LANES | NO_LANES) == 32 | 8:
+        # lane-group / lane tiers from K16 up: records written at even antidiagonals
         # take the first-step-in-fetch() path, and it was exercised here
         assert even_resumes > 0
 

@@ -16,8 +16,11 @@ from helpers import blosum62, result_rows_equal
 
 pytestmark = pytest.mark.gpu
 
-FLAGS = [0, 1, 2, 128, 128 | 64, 32, 64, 16, 4096, 8192] + [8 | (t << 8) for t in range(10)] + \
-        [32 | 8 | (t << 8) for t in range(5)] + [64 | 8 | (t << 8) for t in range(5)]
+# 16384 / 32768: the lane tiers (8 lanes per unit) / the 4-lane groups for every
+# several-lanes-per-unit launch
+FLAGS = [0, 1, 2, 128, 128 | 64, 32 | 16384, 32 | 32768, 64, 16, 4096, 8192] + [8 | (t << 8) for t in range(10)] + \
+        [32 | 8 | (t << 8) | 32768 for t in range(5)] + [32 | 8 | (t << 8) | 16384 for t in range(5)] + \
+        [64 | 8 | (t << 8) for t in range(5)]
 
 
 def _mutate(rng, s, alpha, rate):
