@@ -1462,14 +1462,7 @@ static int run_cascade(xb_batch* B, DevBatch& D) {
             const int* gocc = D.group_fam == 2 && t0 < kNarrowTiers ? D.locc : D.gocc;
             int per_sm = D.all_group ? gocc[t0] : D.occ[t0];
             if (D.all_group && t0 < kNarrowTiers) per_sm = std::min(per_sm, latency_blocks_per_sm(D));
-            int blocks = D.sm_count * per_sm;
-            // one thread per unit: no more threads than units, so that a small
-            // batch fills whole warps on few SMSPs instead of a quarter of the
-            // lanes of every resident warp
-            if (const char* e = std::getenv("XB_THREAD_GRID_CAP"); e && !D.all_group && t0 < kNarrowTiers) {
-                const int cap = std::atoi(e);
-                blocks = int(std::min<int64_t>(blocks, cap > 1 ? cap : std::max<int64_t>(1, D.n_units / kTB)));
-            }
+            const int blocks = D.sm_count * per_sm;
             CK(launch_tier(D.all_group ? D.group_fam : 0, mode, t0, tp, blocks, D.stream));
         } else {  // throughput: one thread per unit (or 8 lanes, wide), the concurrent consumer beside it
             if (concurrent) {

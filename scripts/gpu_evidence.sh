@@ -14,3 +14,8 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 1200 ncu --set full --clock-control none --kernel-name-base mangled -k regex:wide_tier_kernelILi128ELi8ELi0E -c 1 -o gpurun_out/prof_wide python scripts/prof_run.py --config 4 --scale 1.0 --x 100 --runs 1 > gpurun_out/ncu_wide.log 2>&1; echo "ncu-wide rc=$?"
 python scripts/ncu_summary.py report gpurun_out/prof_wide.ncu-rep gpurun_out/r2_wide_k128_config4_x100.txt; rm -f gpurun_out/prof_wide.ncu-rep
 timeout 1500 python scripts/config_report.py --out gpurun_out/r2_configs > gpurun_out/configs.log 2>&1; echo "configs rc=$?"
+# lane tiers (xb_lane.cu): config 1 runs on them; summary of one full capture, and the
+# longest task alone under both several-lanes-per-unit families (cycles per antidiagonal)
+timeout 600 ncu --set full --clock-control none -k regex:lane_tier -c 1 -o gpurun_out/prof_lane python scripts/prof_run.py --config 1 --scale 1.0 --runs 1 > gpurun_out/ncu_lane.log 2>&1; echo "ncu-lane rc=$?"
+python scripts/ncu_summary.py report gpurun_out/prof_lane.ncu-rep gpurun_out/r2_lane_k16_config1.txt; rm -f gpurun_out/prof_lane.ncu-rep
+for fam in 4 8; do echo "== XB_GROUP_FAMILY=$fam"; XB_GROUP_FAMILY=$fam timeout 600 python scripts/lat_probe.py --configs 1,2,3 --settings default,g0,g2; done > gpurun_out/r2_lat_probe.txt 2>&1
