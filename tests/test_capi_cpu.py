@@ -24,6 +24,22 @@ def test_exports_match_header():
     assert L.xb_version().decode().startswith("xdrop_b200")
 
 
+def test_flag_constants_match_header():
+    """The Python binding's XB_FLAG_* / tier constants are the header's."""
+    hdr = open(capi.os.path.join(capi.os.path.dirname(capi.HERE), "include", "xdrop_b200.h")).read()
+    flags = dict(re.findall(r"#define\s+(XB_FLAG_[A-Z_]+)\s+(\d+)", hdr))
+    assert {"XB_FLAG_LANES", "XB_FLAG_NO_LANES", "XB_FLAG_GROUP", "XB_FLAG_LOCALITY"} <= set(flags)
+    for name, val in flags.items():
+        assert getattr(capi, name) == int(val), name
+    assert len(set(flags.values())) == len(flags)  # distinct bits
+    assert capi.NUM_TIERS == int(re.search(r"#define\s+XB_NUM_TIERS\s+(\d+)", hdr).group(1))
+    # the kernel a tier ran on, as the reports name it
+    st = {"start_tier": 0, "start_lane_groups": 2}
+    assert capi.tier_kernel_name(0, st) == "lane_k16"
+    assert capi.tier_kernel_name(0, {"start_tier": 0, "start_lane_groups": 1}) == "group_k16"
+    assert capi.tier_kernel_name(1, {"start_tier": 1, "start_lane_groups": 0}) == "thread_k24"
+
+
 def test_parse_submatrix_matches_reference():
     a, c = blosum62()  # produced by the reference's parse_submatrix
     m = xb.parse_submatrix(synth.blosum62_text())
