@@ -249,10 +249,14 @@ __device__ __forceinline__ void gfinish(GState<K, G, MODE>& S, const TierParams&
                 entry = got;
             }
         }
+        __syncwarp(gmask);
         if (lane == 0) {
+            // a concurrent consumer may take the entry as soon as it is written:
+            // the record first, then the slot, then the entry (volatile)
+            __threadfence();
             const unsigned long long slot = atomicAdd(sk.esc_len, 1ull);
             XB_ASSERT(slot < P.ck_units, kChkList);
-            sk.esc_list[slot] = entry;
+            *(volatile uint32_t*)&sk.esc_list[slot] = entry;
             ++sk.esc;
         }
         return;
