@@ -810,6 +810,9 @@ struct DevBatch {
     TierParams tp{};           // planned launch parameters (run_plan -> run_cascade)
     bool all_group = false, no_group = false;
     int group_fam = 1;  // several-lanes-per-unit launches of the narrow tiers: 1 = 4-lane groups, 2 = lane tiers
+    // small batches only (at most kPlanUnits units): the longest unit's and the
+    // whole batch's estimated antidiagonals (unit_est), for the family choice
+    double est_max = 0, est_sum = 0;
     Workspace* ws = nullptr;
     DevPool* pool = nullptr;
     std::vector<int64_t> tasks;  // global task (or unit) indices of this shard
@@ -1078,6 +1081,27 @@ static int upload_inputs(xb_batch* B, DevBatch& D, const void* items) {
 
 constexpr int kGroupLanes = 4;  // lanes per unit in the lane-group tiers (xb_group.cu)
 constexpr int kLaneLanes = 8;   // lanes per unit in the lane tiers (xb_lane.cu)
+// Batches of at most this many units are planned with host-side estimates of
+// their work (est_sum / est_max); every latency-planned batch is smaller.
+constexpr int64_t kPlanUnits = 1 << 16;
+
+// 4-lane groups (1) or lane tiers (2) for a latency-planned batch of nu
+// units.  Both families finish when the longest unit does or when the
+// machine is through the work, whichever is later; in cycles of SMSP time,
+// measured on configs 1-3 at several scales:
+//   groups: a step every 490 cycles with one warp per SMSP, 620 with two;
+//           33 cycles of issue per unit and antidiagonal
+//   lanes:  300 / 450 cycles per step; 55 (DNA) or 62 (table modes) of issue
+template <typename DB>
+static int pick_group_family(const DB& D, bool table_mode, int64_t nu) {
+    const double sm = double(D.sm_count), smsp = 4.0 * sm;
+    if (D.est_max <= 0) return nu <= int64_t(D.sm_count) * 16 ? 2 : 1;
+    const double over = std::min(1.0, std::max(0.0, (double(nu) - 32.0 * sm) / (32.0 * sm)));
+    const double groups = std::max((490.0 + 130.0 * over) * D.est_max, 33.0 * D.est_sum / smsp);
+    const double lanes = std::max((double(nu) <= 16.0 * sm ? 300.0 : 450.0) * D.est_max,
+                                  (table_mode ? 62.0 : 55.0) * D.est_sum / smsp);
+    return lanes < 0.95 * groups ? 2 : 1;
+}
 static int family_lanes(int fam) { return fam == 2 ? kLaneLanes : fam == 1 ? kGroupLanes : 1; }
 
 // Kernel families of the narrow tiers (K16..K64): 0 = one thread per unit,
@@ -1322,7 +1346,7 @@ static int run_plan(xb_batch* B, DevBatch& D) {
     // (config 3: 3.4 ms against 3.8 ms, config 2: 6.4 against 11 ms)
     D.group_fam = (B->flags & XB_FLAG_LANES) ? 2 : (B->flags & XB_FLAG_NO_LANES) ? 1
                   : forced_group_family() ? forced_group_family()
-                  : (latency_mode && nu <= int64_t(D.sm_count) * (kTB / kLaneLanes)) ? 2 : 1;
+                  : latency_mode ? pick_group_family(D, mode != 0, nu) : 1;
     D.t0 = forced >= 0 ? forced : (pn > 0 ? -1 : default_start);  // -1: read back after the pilot
     return XB_OK;  // a pilot-chosen start tier arrives in h_misc[kMiscStartTier] (written by the kernel)
 }
@@ -1773,6 +1797,20 @@ xb_batch* xb_batch_create(xb_pool* p, const xb_task* tasks, int64_t n, int k, in
             shard_lpt(cost, int(ids.size()), sh);
         for (size_t g = 0; g < ids.size(); ++g) B->devs[g].tasks = std::move(sh[g]);
     }
+    for (size_t g = 0; g < ids.size(); ++g) {  // planning estimates of small batches
+        DevBatch& D = B->devs[g];
+        const int64_t ni = ids.size() > 1 ? int64_t(D.tasks.size()) : n;
+        if (2 * ni > kPlanUnits) continue;
+        for (int64_t q = 0; q < ni; ++q) {
+            const xb_task& t = tasks[ids.size() > 1 ? D.tasks[size_t(q)] : q];
+            const long long hl = p->offsets[t.h_id + 1] - p->offsets[t.h_id];
+            const long long vl = p->offsets[t.v_id + 1] - p->offsets[t.v_id];
+            const long long l = unit_est((long long)t.h_seed, (long long)t.v_seed);
+            const long long r = unit_est(hl - (long long)t.h_seed - k, vl - (long long)t.v_seed - k);
+            D.est_sum += double(l + r);
+            D.est_max = std::max(D.est_max, double(std::max(l, r)));
+        }
+    }
     lk.unlock();
     for (size_t g = 0; g < ids.size(); ++g) {
         DevBatch& D = B->devs[g];
@@ -1993,6 +2031,12 @@ int xb_extend_units(xb_pool* p, const xb_unit* units, int64_t n, int band, xb_si
         }
         D.n_items = int64_t(D.h_units.size());
         D.n_units = D.n_items;
+        if (D.n_units <= kPlanUnits)
+            for (const DevUnit& x : D.h_units) {
+                const long long e = unit_est(x.h_len, x.v_len);
+                D.est_sum += double(e);
+                D.est_max = std::max(D.est_max, double(e));
+            }
         rc = setup_device(B, D, exec, units);
         if (!rc) rc = upload_inputs(B, D, nullptr);
         if (rc) {
