@@ -87,6 +87,7 @@ struct LState {
     // step must then take the exact width test)
     uint32_t m_above, m_ge;
     int32_t narrow;
+    uint32_t ones;               // 0x01010101
     uint32_t Z[4];               // MODE 0: match bytes of the coming step (see the thread tier)
     uint32_t VW, HW;             // 2-bit windows of this lane's S slots (MODE 0)
     uint32_t VWb[NB], HWb[NB];   // byte windows (table modes)
@@ -99,7 +100,7 @@ struct LState {
 template <int K, int G, int MODE>
 __device__ __forceinline__ void l_limits(LState<K, G, MODE>& S) {
     S.d_vm = min(2 * (S.ubase + S.n + 1), 2 * (S.m - S.ubase - K + 2) - 1);
-    S.d_lim = min(S.d_vm, min(S.n + S.m + 2, S.dcap + 1));
+    S.d_lim = S.narrow ? INT_MIN : min(S.d_vm, min(S.n + S.m + 2, S.dcap + 1));  // feeds the step trigger only
 }
 
 template <int K, int G, int MODE>
@@ -343,9 +344,15 @@ template <int K, int G, int MODE>
 __device__ __forceinline__ void l_match(LState<K, G, MODE>& S, uint32_t inv) {
     if constexpr (MODE == 0) {
         const uint32_t x = llop3<0xBE>(S.VW, S.HW, inv);  // (a ^ b) | c
-        const uint32_t z = ~(x | (x << 1));
+        const uint32_t z = llop3<0x03>(x, x << 1, 0u);    // ~(a | b)
+        // (z >> 2q) & 0x02020202 | 0x01010101 as one LOP3 each: the second
+        // constant comes in a register (S.ones)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) S.Z[q] = ((z >> (2 * q)) & 0x02020202u) | 0x01010101u;
+        for (int q = 0; q < 4; ++q) {
+            uint32_t r;
+            asm("lop3.b32 %0, %1, 0x02020202, %2, 0xEA;" : "=r"(r) : "r"(z >> (2 * q)), "r"(S.ones));  // (a & b) | c
+            S.Z[q] = r;
+        }
     }
 }
 
@@ -511,7 +518,7 @@ __device__ __forceinline__ bool lstep(LState<K, G, MODE>& S, int32_t (&cur)[K / 
     {
         const bool edge_may = ODD ? (lane == G - 1 && cand[SS - 1] >= S.Tv) : (lane == 0 && cand[0] >= S.Tv);
         const unsigned bl = __ballot_sync(smask, lm >= S.Tv);
-        trig = (edge_may | ((bl & gmask) == 0u) | (d + 1 >= S.d_lim) | (S.narrow != 0)) & (S.stop == 0);
+        trig = (edge_may | ((bl & gmask) == 0u) | (d + 1 >= S.d_lim)) & (S.stop == 0);  // d_lim: also band < K
     }
     // the lane's own chain from Tv, before the lanes above are known
     // (align.cpp:122-129 in ascending i = descending slot): c_s, and whether
@@ -568,13 +575,14 @@ __device__ __forceinline__ bool lstep(LState<K, G, MODE>& S, int32_t (&cur)[K / 
         const bool none = ODD ? lane == 0 : lane == G - 1;
         S.edge = (nraw >= nthr && !none) ? nraw : kDeadS;
     }
-    // drop test, kill, live bits
+    // drop test, kill, live bits (a kept cell is >= Tv >= 1, the dead marker
+    // negative: the dead mask is the rows' sign bits, shifted in slot by slot)
     uint32_t dm = 0u;
 #pragma unroll
     for (int s = SS - 1; s >= 0; --s) {
         const bool dead = dead0[s] || cand[s] < c0;
         cur[s] = dead ? kDeadS : cand[s];
-        dm |= dead ? (1u << s) : 0u;
+        dm = __funnelshift_l(uint32_t(cur[s]), dm, 1);
     }
     const uint32_t lv = ~dm & vml;
     // gather the live bits of row d (consumed a step later)
@@ -652,7 +660,8 @@ __global__ void __launch_bounds__(128) lane_tier_kernel(TierParams P) {
     S.m_above = (gmask << 1 << lane) & gmask;
     S.m_ge = S.m_above | (1u << wl);
     S.narrow = P.band < K ? 1 : 0;
-    asm volatile("" : "+r"(S.m_above), "+r"(S.m_ge), "+r"(S.narrow));
+    S.ones = P.ones;
+    asm volatile("" : "+r"(S.m_above), "+r"(S.m_ge), "+r"(S.narrow), "+r"(S.ones));
 #pragma unroll
     for (int q = 0; q < 4; ++q) S.Z[q] = 0x01010101u;
     S.Tv = 0;
