@@ -210,6 +210,14 @@ int xb_measure_int32_peak(int device, double* alu_ops_per_clk_sm, double* mixed_
  * return -1 (checks compiled out). */
 int xb_debug_checks(int device, uint32_t* failed);
 
+/* The planner's choice for a latency-planned batch (no reference analogue; the
+ * reference schedules IPU tiles, partition.cpp:231-305): which kernels run
+ * several lanes per unit -- 1 = 4-lane groups, 2 = lane tiers (8 lanes) --
+ * given the SM count, the scoring mode (0 = +1/-1/-1 DNA, else table), the
+ * number of units and the estimated antidiagonals of the longest unit and of
+ * the whole batch.  Pure host arithmetic: no device needed. */
+int xb_plan_group_family(int sm_count, int table_mode, int64_t n_units, double est_max, double est_sum);
+
 /* ---- deterministic synthetic configs (BASELINE.json configs[0..4]) ---- */
 /* Builds config `cfg` (1..5) at `scale` (1.0 = the BASELINE size).  Returns
  * a handle; query sizes then copy out.  Matrix configs (cfg 3) take the

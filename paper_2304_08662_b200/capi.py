@@ -144,6 +144,7 @@ def lib() -> C.CDLL:
         "xb_last_stats": (I, [C.POINTER(XbStats)]),
         "xb_shard_tasks": (I, [P, P, I64, I, I, I, P, C.POINTER(I64)]),
         "xb_debug_checks": (I, [I, C.POINTER(C.c_uint32)]),
+        "xb_plan_group_family": (I, [I, I, I64, C.c_double, C.c_double]),
         "xb_measure_int32_peak": (I, [I, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                       C.POINTER(C.c_double), C.POINTER(I)]),
         "xb_synth_make": (P, [I, C.c_double, C.c_uint64, C.c_char_p, I, C.POINTER(I)]),
@@ -180,7 +181,7 @@ EXPORTED = ["xb_version", "xb_strerror", "xb_device_count", "xb_scheme_match_mis
             "xb_last_stats", "xb_measure_int32_peak", "xb_synth_make", "xb_synth_sizes",
             "xb_synth_copy", "xb_synth_free", "xb_synth_pairs", "xb_sweep_band", "xb_fasta_parse",
             "xb_fasta_sizes", "xb_fasta_copy", "xb_pool_add_fasta", "xb_fasta_free", "xb_parse_seeds",
-            "xb_parse_overlaps", "xb_shard_tasks", "xb_debug_checks"]
+            "xb_parse_overlaps", "xb_shard_tasks", "xb_debug_checks", "xb_plan_group_family"]
 
 
 class XbParseError(C.Structure):

@@ -2129,6 +2129,11 @@ int xb_shard_tasks(xb_pool* p, const xb_task* tasks, int64_t n, int k, int n_sha
     return XB_OK;
 }
 
+int xb_plan_group_family(int sm_count, int table_mode, int64_t n_units, double est_max, double est_sum) {
+    struct { int sm_count; double est_max, est_sum; } d{sm_count, est_max, est_sum};
+    return pick_group_family(d, table_mode != 0, n_units);
+}
+
 int xb_debug_checks(int device, uint32_t* failed) {
     if (failed) *failed = 0;
 #if XB_CHECKS

@@ -40,6 +40,28 @@ def test_flag_constants_match_header():
     assert capi.tier_kernel_name(1, {"start_tier": 1, "start_lane_groups": 0}) == "thread_k24"
 
 
+def test_plan_group_family():
+    """The planner's choice between the 4-lane groups (1) and the lane tiers (2)
+    for latency-planned batches, at the points measured on a 148-SM B200
+    (DESIGN.md 4.2b): est_max = the longest unit's antidiagonals, est_sum = the
+    batch's."""
+    L = capi.lib()
+    f = lambda table, nu, lmax, total: L.xb_plan_group_family(148, table, nu, float(lmax), float(total))
+    # config 1 (1,000-antidiagonal units) at x1, x2, x3, x4
+    assert [f(0, n, 990, 990 * n) for n in (2000, 4000, 6000, 8000)] == [2, 2, 1, 1]
+    # config 2 (uniform up to 20,000) at x0.1 .. x1
+    assert [f(0, n, 20000, 10000 * n) for n in (2000, 4000, 8000, 12000, 16000, 20000)] == [2, 2, 2, 2, 1, 1]
+    # config 3 (protein, table mode, up to ~9,930) at x0.1 .. x1
+    assert [f(1, n, 9930, 2950 * n) for n in (2000, 4000, 8000, 12000, 16000, 20000)] == [2, 2, 2, 2, 2, 1]
+    # a single task is pure latency; no estimate falls back to the unit count
+    assert f(0, 2, 20000, 30000) == 2 and f(1, 2, 5000, 8000) == 2
+    assert f(0, 2000, 0, 0) == 2 and f(0, 20000, 0, 0) == 1
+    # more work at the same longest unit never moves a batch to the lane tiers
+    for nu in (3000, 9000, 30000):
+        picks = [f(0, nu, 10000, w) for w in (1e6, 1e7, 1e8, 1e9, 1e10)]
+        assert picks == sorted(picks, reverse=True), picks
+
+
 def test_parse_submatrix_matches_reference():
     a, c = blosum62()  # produced by the reference's parse_submatrix
     m = xb.parse_submatrix(synth.blosum62_text())
